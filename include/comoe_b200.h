@@ -1,0 +1,168 @@
+/* comoe_b200.h — C ABI of the B200-native CoMoE MoE-layer hot path.
+ *
+ * Every entry point takes raw device pointers, sizes and a cudaStream_t
+ * (passed as void*), enqueues asynchronous work on that stream, never
+ * allocates, never synchronises the device, and returns 0 on success or a
+ * negative status (see COMOE_E*) with a message in comoe_last_error().
+ * Buffers are owned by the caller (the Python host layer allocates them with
+ * PyTorch). Kernels are sm_100a only.
+ *
+ * The reference (pkg/src/comoe, pure Python/NumPy) has no FFI; each function
+ * below cites the reference function whose behaviour it implements or the
+ * analytic charge it replaces. Ties always go to the lowest index (reference
+ * convention, pkg/src/comoe/aggregation.py:165,193).
+ */
+#ifndef COMOE_B200_H_
+#define COMOE_B200_H_
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define COMOE_B200_ABI_VERSION 1
+
+/* status codes */
+#define COMOE_OK 0
+#define COMOE_EBADARG (-1)
+#define COMOE_EUNSUPPORTED (-2)
+#define COMOE_ECUDA (-3)
+#define COMOE_ENODRIVER (-4)
+
+/* activations of the expert FFN */
+#define COMOE_ACT_RELU 0   /* Switch: relu(x Wi^T) Wo^T                       */
+#define COMOE_ACT_SWIGLU 1 /* Mixtral: (silu(x W1^T) * (x W3^T)) W2^T          */
+
+/* grouped-GEMM epilogues */
+#define COMOE_EPI_RELU 0
+#define COMOE_EPI_SWIGLU 1
+#define COMOE_EPI_SCALE_SCATTER 2
+#define COMOE_EPI_STORE 3
+
+/* element types for merge / similarity */
+#define COMOE_DTYPE_BF16 0
+#define COMOE_DTYPE_F64 1
+
+/* ---------------------------------------------------------------- misc */
+int comoe_version(void);
+const char* comoe_last_error(void);
+int comoe_num_sms(int device);
+
+/* ---------------------------------------------------------------- K1 gate
+ * Replaces the synthetic routing source generate_routing
+ * (pkg/src/comoe/moe.py:186-230) with a real fp32 router, and applies
+ * ModelVariant.resolve (pkg/src/comoe/aggregation.py:101-103) as `slot_map`.
+ *
+ * comoe_gate_prepare: split the fp32 router Wg[d,E] (row-major, x @ Wg) into
+ *   three bf16 terms wg_split[3][EP][d] (EP = comoe_gate_padded_experts(E)).
+ * comoe_gate_topk: for each token t of x[T,d] (bf16): logits = x_t . Wg (fp32,
+ *   tensor cores), top-k on the logits (k in {1,2}), probabilities
+ *   (norm_topk=0: softmax over all E; 1: renormalised over the k picks),
+ *   group = slot_map[expert] (identity if NULL; when both picks map to one
+ *   group the second is folded into the first), token-order rank inside its
+ *   128-token tile, and the per-tile group histogram tile_hist[k][ntiles][G].
+ *   logits_out[T,E] is optional (NULL to skip).
+ */
+int comoe_gate_padded_experts(int E);
+int comoe_gate_num_tiles(int T);
+int comoe_gate_prepare(const float* wg, int d, int E, void* wg_split, void* stream);
+int comoe_gate_topk(const void* x, int T, int d, const void* wg_split, int E, int top_k,
+                    int norm_topk, const int* slot_map, int n_groups, float* logits_out,
+                    int* expert_idx, int* group_idx, float* gate_prob, int* local_rank,
+                    int* tile_hist, void* stream);
+
+/* ---------------------------------------------------------------- routing scan
+ * Capacity in stream order (first choices in token order, then second
+ * choices): tile_offset = exclusive scan of tile_hist per group,
+ * group_count = assignments per group (pre-capacity; the per-group analogue
+ * of collect_stats, pkg/src/comoe/moe.py:250-262), group_kept =
+ * min(count, capacity), group_base = exclusive scan of group_kept.
+ */
+int comoe_route_scan(const int* tile_hist, int top_k, int ntiles, int G, int capacity,
+                     int* tile_offset, int* group_count, int* group_kept, int* group_base,
+                     void* stream);
+/* counts[E] = histogram of original expert indices (collect_stats, moe.py:250-262) */
+int comoe_expert_histogram(const int* expert_idx, long n, int E, int* counts, void* stream);
+
+/* ---------------------------------------------------------------- K2 permute
+ * Kept assignments are copied to x_perm[group_base[g] + rank] (expert-sorted,
+ * compact); row_token/row_prob describe each row; token_pos[T,k] = row or -1.
+ * If y_zero != NULL, rows of tokens with no kept assignment are zeroed there
+ * (the top-1 fused-combine output).
+ */
+int comoe_permute(const void* x, int T, int d, int top_k, const int* group_idx,
+                  const float* gate_prob, const int* local_rank, const int* tile_offset,
+                  const int* group_base, int n_groups, int capacity, void* x_perm,
+                  int* row_token, float* row_prob, int* token_pos, void* y_zero, void* stream);
+
+/* ---------------------------------------------------------------- K3 expert FFN
+ * Replaces the analytic expert charge (pkg/src/comoe/simulator.py:705,
+ * scenario.py:471 expert_flops) with tcgen05 grouped GEMMs over the HBM
+ * expert slot pool: slot s holds [W_in (N1 x d) | W_out (d x d_ff)] bf16,
+ * N1 = d_ff (ReLU) or 2*d_ff (SwiGLU, gate/up interleaved in 128-row blocks).
+ * Group g covers rows [group_row_base[g], +group_rows[g]) of x_perm and uses
+ * slot group_slot[g]. h_work[total_rows, d_ff] is scratch. If row_token is
+ * given, the second GEMM scales by row_prob and scatters rows to
+ * out[row_token[r]] (fused top-1 combine); otherwise it stores rows in place.
+ * Requires d, d_ff multiples of 256 and of 64.
+ */
+int comoe_grouped_gemm(const void* a, long a_rows, const void* pool, int n_slots, long slot_stride,
+                       long b_offset, int N, int K, const int* group_rows,
+                       const int* group_row_base, const int* group_slot, int G, int epi_mode,
+                       void* out, int ldo, const int* row_token, const float* row_prob,
+                       void* stream);
+int comoe_grouped_ffn(const void* x_perm, long total_rows, int d, int d_ff, int act,
+                      const void* pool, int n_slots, long slot_stride, const int* group_rows,
+                      const int* group_row_base, const int* group_slot, int G, void* h_work,
+                      void* out, int ldo, const int* row_token, const float* row_prob,
+                      void* stream);
+
+/* ---------------------------------------------------------------- K4 combine
+ * y[t] = sum_j gate_prob[t,j] * y_perm[token_pos[t,j]] (token_pos -1 -> 0).
+ */
+int comoe_combine(const void* y_perm, const int* token_pos, const float* gate_prob, int T, int d,
+                  int top_k, void* y, void* stream);
+
+/* ---------------------------------------------------------------- K5 merge
+ * merge_group (pkg/src/comoe/aggregation.py:200-215) for n_groups groups in
+ * one launch: out[g] = (sum_{j in g} weights[j] * member[j]) / divisor[g].
+ * Host passes weights = f_j, divisor = sum f (or 1 and n for the
+ * zero-frequency plain mean). F64 reproduces numpy's order bit-exactly.
+ * All pointer tables live in device memory.
+ */
+int comoe_merge(int dtype, const void* const* member_ptrs, const int* group_offsets,
+                const double* weights, const double* divisor, void* const* out_ptrs, int n_groups,
+                int max_members, long D, void* stream);
+
+/* ---------------------------------------------------------------- K6 similarity
+ * similarity_matrix (pkg/src/comoe/moe.py:339-365) in two device stages:
+ * comoe_sim_contract: gram[E,E] = P P^T and logits[E,n,B] =
+ *   sum_d probes[n,d] P[e,d] proj[b,d] (the einsum at moe.py:351), split-K
+ *   over D with a deterministic reduction; rows are expert vectors (bf16 or
+ *   f64, by dtype); probes/proj are f64 [n,D] / [B,D]; work is scratch of
+ *   comoe_sim_workspace_bytes(E, n, B, D) bytes.
+ * comoe_sim_finalize: S = alpha*cos + (1-alpha)*clip(1 - meanKL, 0, 1) with
+ *   log-softmax surrogate distributions (finite where the reference NaNs).
+ */
+long comoe_sim_workspace_bytes(int E, int n_probes, int buckets, long D);
+int comoe_sim_contract(int dtype, const void* const* rows, int E, long D, const double* probes,
+                       int n_probes, const double* proj, int buckets, double* gram,
+                       double* logits, void* work, void* stream);
+int comoe_sim_finalize(const double* gram, const double* logits, int E, int n_probes, int buckets,
+                       double alpha, double* sim, void* stream);
+
+/* ---------------------------------------------------------------- K8 predictor
+ * PredictorMLP.forward_batch (pkg/src/comoe/offload.py:147-154) with the
+ * input built as in predict_next_layer (offload.py:157-172): x = [K-hot of
+ * slots[t] over E | emb[t] | ctx[t]]; probs = softmax(W2 relu(W1 x + b1) + b2).
+ * f64 throughout. demand[E] (optional) = sum_t probs[t] in token order.
+ */
+int comoe_predictor_mlp(const int* slots, int B, int K, const double* emb, int emb_dim,
+                        const double* ctx, int ctx_dim, const double* w1, const double* b1,
+                        int hidden, const double* w2, const double* b2, int E, double* probs,
+                        double* demand, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* COMOE_B200_H_ */

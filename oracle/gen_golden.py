@@ -1,0 +1,225 @@
+"""Generate golden fixtures from the UNMODIFIED reference package.
+
+Run in the build container (where /root/reference exists):
+    python oracle/gen_golden.py
+It imports comoe from /root/reference/pkg/src (read-only; nothing is copied)
+and writes small JSON fixtures to tests/golden/. The GPU box never runs this;
+tests there read the committed fixtures only.
+
+Fixtures
+  fusion_cases.json    per-layer fusion pipeline cases: inputs (freqs, params,
+                       calibration) and the reference's similarity matrix,
+                       principals, grouping, merged params, slot_map, score
+  merge_hand.json      the reference unit-test hand cases for merge_group
+  merge_bigsum.json    seeded large merges (D up to 4,718,592): sha256 of the
+                       reference merge_group output bytes (fp64), for the
+                       device fp64 bit-exactness check
+  policy_cases.json    cache-policy decisions: prefetch_threshold, eviction
+                       scores, evict victims / infeasible, decide_prefetch,
+                       plan_initial_placement, correct_misprediction
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+
+REF = Path("/root/reference/pkg/src")
+OUT = Path(__file__).resolve().parent.parent / "tests" / "golden"
+
+
+def _ref():
+    sys.path.insert(0, str(REF))
+    import comoe  # noqa: F401
+    from comoe import aggregation, moe, offload
+    return moe, aggregation, offload
+
+
+def fusion_cases(moe, agg, n_cases=40):
+    rng = np.random.default_rng(20260901)
+    cases = []
+    for i in range(n_cases):
+        E = int(rng.integers(2, 17))
+        dim = int(rng.choice([6, 16, 64]))
+        spec = moe.MoeModelSpec(total_layers=2, encoder_moe_layers=(1,), decoder_moe_layers=(),
+                                experts_per_layer=E, expert_size_bytes=1e6, top_k=1,
+                                expert_param_dim=dim)
+        model = moe.synthesize_model(spec, int(rng.integers(0, 2 ** 31)))
+        counts = rng.integers(0, 50, size=E).astype(float)
+        if i % 7 == 3:
+            counts[:] = 0.0
+            counts[0] = 1.0   # one active expert -> zero-frequency groups
+        if counts.sum() == 0:
+            counts[0] = 1.0
+        if i % 5 == 2:
+            counts[1 % E] = counts[0]  # frequency ties
+        stats = moe.ActivationStats(counts={1: counts}, totals={1: int(counts.sum())},
+                                    experts_per_layer=E)
+        calib = moe.make_calibration(dim, n_probes=int(rng.integers(1, 9)),
+                                     seed=int(rng.integers(0, 1000)),
+                                     buckets=int(rng.integers(2, 9)))
+        alpha = float(rng.choice([0.0, 0.5, 1.0, 0.3]))
+        r = float(rng.choice([0.25, 0.5, 0.75]))
+        theta = float(rng.choice([0.0, 0.0, 0.1, 0.3]))
+        cfg = agg.FusionConfig(mode="fixed", r=r, theta_act=theta)
+        experts = model.layer_experts(1)
+        S = moe.similarity_matrix(experts, alpha, calib)
+        target = agg.fixed_retention(E, r)
+        princ = agg.identify_principals(stats, 1, target, theta)
+        groups = agg.group_experts(experts, princ, S)
+        by_slot = {e.slot: e for e in experts}
+        merged = {g.principal_slot: agg.merge_group(g, by_slot, stats, 1).params.tolist()
+                  for g in groups}
+        var = agg.fuse_model(model, stats, cfg, alpha, calib)
+        h, hbar = agg.layer_entropy(stats, 1)
+        cases.append(dict(
+            E=E, dim=dim, counts=counts.tolist(), alpha=alpha, r=r, theta_act=theta,
+            params=[e.params.tolist() for e in experts],
+            probes=calib.probes.tolist(), projection=calib.projection.tolist(),
+            sim=S.tolist(), target=target, principals=princ,
+            groups={str(g.principal_slot): list(g.member_slots) for g in groups},
+            merged={str(k): v for k, v in merged.items()},
+            slot_map={str(k): v for k, v in var.slot_map[1].items()},
+            perf_estimate=var.perf_estimate, entropy=h, hbar=hbar,
+            adaptive=agg.adaptive_retention(E, 0.25, 0.3, hbar, 1)))
+    return cases
+
+
+def merge_hand(moe, agg):
+    Ex = moe.Expert
+    out = []
+    by = {0: Ex(1, 0, np.array([2.0, 0.0]), 3.0), 1: Ex(1, 1, np.array([0.0, 4.0]), 3.0)}
+    st = moe.ActivationStats(counts={1: np.array([3.0, 1.0])}, totals={1: 4},
+                             experts_per_layer=2)
+    m = agg.merge_group(agg.ExpertGroup(0, (1,)), by, st, 1)
+    out.append(dict(vectors=[[2.0, 0.0], [0.0, 4.0]], freqs=[0.75, 0.25], expected=m.params.tolist()))
+    st0 = moe.ActivationStats(counts={1: np.zeros(2)}, totals={1: 10}, experts_per_layer=2)
+    m0 = agg.merge_group(agg.ExpertGroup(0, (1,)), by, st0, 1)
+    out.append(dict(vectors=[[2.0, 0.0], [0.0, 4.0]], freqs=[0.0, 0.0], expected=m0.params.tolist()))
+    return out
+
+
+def merge_bigsum(moe, agg):
+    """Seeded large groups; the device must reproduce the bytes exactly."""
+    out = []
+    for seed, n, D in ((11, 2, 4_718_592), (12, 4, 1_000_003), (13, 9, 262_144), (14, 3, 65_537)):
+        rng = np.random.default_rng(seed)
+        V = rng.normal(size=(n, D)) * 0.02
+        f = rng.integers(0, 100, size=n).astype(float)
+        if seed == 14:
+            f[:] = 0.0
+        total = float(f.sum()) if f.sum() > 0 else 1.0
+        experts = {s: moe.Expert(1, s, V[s], 1.0) for s in range(n)}
+        st = moe.ActivationStats(counts={1: f}, totals={1: max(int(f.sum()), 1)},
+                                 experts_per_layer=n)
+        g = agg.ExpertGroup(0, tuple(range(1, n)))
+        m = agg.merge_group(g, experts, st, 1).params
+        out.append(dict(seed=seed, n=n, D=D, counts=f.tolist(), total=total,
+                        sha256=hashlib.sha256(np.ascontiguousarray(m).tobytes()).hexdigest(),
+                        head=m[:4].tolist()))
+    return out
+
+
+def policy_cases(off, n_cases=60):
+    rng = np.random.default_rng(777)
+    cases = []
+    for i in range(n_cases):
+        E = int(rng.integers(3, 12))
+        layers = int(rng.integers(1, 3))
+        experts = [(l, s) for l in range(layers) for s in range(E)]
+        sizes = {e: float(rng.choice([1.0, 1.5, 2.0])) for e in experts}
+        ws_cap = float(rng.choice([2.0, 3.0, 4.0]))
+        ca_cap = float(rng.choice([3.0, 5.0, 8.0]))
+        freqs = {e: float(rng.random()) for e in experts}
+        if i % 4 == 0:
+            for e in experts[:3]:
+                freqs[e] = 0.5  # ties
+        pinned = set()
+        if i % 3 == 0:
+            pinned = {experts[int(rng.integers(0, len(experts)))]}
+        try:
+            plan = off.plan_initial_placement(sizes, freqs, ws_cap, ca_cap, pinned=frozenset(pinned),
+                                              working_set_bytes=1.0)
+            placement = {f"{e[0]},{e[1]}": t for e, t in plan.assignment.items()}
+            order = [list(e) for e in plan.order]
+            eta = plan.eta_gs
+            state = off.build_cache_state(plan, sizes, ws_cap, ca_cap, pinned=pinned)
+            infeasible_place = False
+        except Exception as exc:  # InfeasibleError
+            placement, order, eta, state = None, None, None, None
+            infeasible_place = type(exc).__name__
+        case = dict(sizes={f"{e[0]},{e[1]}": v for e, v in sizes.items()},
+                    freqs={f"{e[0]},{e[1]}": v for e, v in freqs.items()},
+                    ws_cap=ws_cap, ca_cap=ca_cap, pinned=[list(e) for e in pinned],
+                    placement=placement, order=order, eta_gs=eta,
+                    placement_error=infeasible_place)
+        if state is not None:
+            scores = {e: float(rng.uniform(0, 3)) for e in state.cache}
+            need = float(rng.uniform(0, ca_cap * 1.2))
+            try:
+                vict = off.evict(state, need, scores)
+                ev = [list(e) for e in vict]
+                ev_err = False
+            except Exception as exc:
+                ev, ev_err = None, type(exc).__name__
+            probs = rng.random(E)
+            if i % 5 == 1:
+                probs[1] = probs[0]
+            theta = float(rng.choice([0.0, 0.2, 0.5, 0.8]))
+            layer = int(rng.integers(0, layers))
+            budget = None if i % 2 else float(rng.uniform(0, 6))
+            pre = off.decide_prefetch(probs, theta, state, layer, lambda e: sizes[e],
+                                      budget_bytes=budget)
+            case.update(cache={f"{e[0]},{e[1]}": v for e, v in state.cache.items()},
+                        workspace={f"{e[0]},{e[1]}": v for e, v in state.workspace.items()},
+                        scores={f"{e[0]},{e[1]}": v for e, v in scores.items()},
+                        bytes_needed=need, evict=ev, evict_error=ev_err,
+                        probs=probs.tolist(), theta=theta, layer=layer, budget=budget,
+                        prefetch=[list(e) for e in pre])
+            # substitution
+            host = sorted(state.host)
+            if host:
+                needed = host[int(rng.integers(0, len(host)))]
+                simv = {e: float(rng.uniform(0.5, 1.0)) for e in experts}
+                pol = off.OffloadPolicy(substitution_sim_min=float(rng.choice([0.7, 0.8, 0.95])))
+                prio = float(rng.random())
+                dec = off.correct_misprediction(needed, state, lambda a, b: simv[b], pol,
+                                                priority=prio, priority_threshold=0.8)
+                case.update(subst=dict(needed=list(needed), sim={f"{e[0]},{e[1]}": v for e, v in simv.items()},
+                                       sim_min=pol.substitution_sim_min, priority=prio,
+                                       action=dec.action, expert=list(dec.expert),
+                                       penalty=dec.penalty))
+        # threshold + score grid
+        pol = off.OffloadPolicy(theta_base=float(rng.uniform(0, 1)), delta_pref=float(rng.random()),
+                                gamma_cachethr=float(rng.random()),
+                                threshold_mode=str(rng.choice(["resource-aware", "storage-fraction", "constant"])),
+                                conservative_stability=bool(i % 2))
+        s_b, m_av, m_tot = float(rng.random()), float(rng.uniform(0, 8e9)), 8e9
+        case["threshold"] = dict(mode=pol.threshold_mode, theta_base=pol.theta_base,
+                                 delta_pref=pol.delta_pref, gamma_cachethr=pol.gamma_cachethr,
+                                 conservative=pol.conservative_stability, s_b=s_b, m_avail=m_av,
+                                 m_total=m_tot, value=off.prefetch_threshold(pol, s_b, m_av, m_tot))
+        args = (float(rng.random()), float(rng.choice([0.0, 1e-9, rng.random() * 4])),
+                float(rng.choice([0.0, rng.random()])), float(rng.random()), float(rng.random()))
+        case["score"] = dict(args=list(args), value=off.eviction_score(*args))
+        cases.append(case)
+    return cases
+
+
+def main():
+    moe, agg, off = _ref()
+    OUT.mkdir(parents=True, exist_ok=True)
+    (OUT / "fusion_cases.json").write_text(json.dumps(fusion_cases(moe, agg)))
+    (OUT / "merge_hand.json").write_text(json.dumps(merge_hand(moe, agg), indent=1))
+    (OUT / "merge_bigsum.json").write_text(json.dumps(merge_bigsum(moe, agg), indent=1))
+    (OUT / "policy_cases.json").write_text(json.dumps(policy_cases(off)))
+    for p in sorted(OUT.glob("*.json")):
+        print(p.name, p.stat().st_size)
+
+
+if __name__ == "__main__":
+    main()

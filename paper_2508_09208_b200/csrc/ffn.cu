@@ -1,0 +1,103 @@
+// K3 entry points: grouped expert GEMM and the two-pass expert FFN over the
+// HBM expert slot pool. One slot holds one expert as a flat bf16 vector
+// [W_in (N1 x d) | W_out (d x d_ff)], N1 = d_ff (ReLU) or 2*d_ff (SwiGLU with
+// gate/up interleaved in 128-row blocks) — the device image of the
+// reference's flat `Expert.params` (pkg/src/comoe/moe.py:69-74).
+#include "grouped_gemm.cuh"
+#include "../../include/comoe_b200.h"
+
+namespace comoe {
+
+template <int BN, int kStages, int kMode>
+static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GroupedGemmParams& p,
+                       cudaStream_t stream) {
+  using S = GemmSmem<BN, kStages>;
+  auto kern = grouped_gemm_kernel<BN, kStages, kMode>;
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kTotal);
+    attr_set = true;
+  }
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  kern<<<sms, kGemmThreads, S::kTotal, stream>>>(ta, tb, p);
+  return check_launch("grouped_gemm_kernel");
+}
+
+// B operand: `N x K` matrix at element offset `b_offset` inside every slot.
+static int grouped_gemm_impl(const void* a, long a_rows, const void* pool, int n_slots,
+                             long slot_stride, long b_offset, int N, int K,
+                             const int* group_rows, const int* group_row_base,
+                             const int* group_slot, int G, int epi_mode, void* out, int ldo,
+                             const int* row_token, const float* row_prob, cudaStream_t stream) {
+  COMOE_REQUIRE(a && pool && out && group_rows && group_row_base && group_slot, kBadArg,
+                "grouped_gemm: null pointer");
+  COMOE_REQUIRE(G >= 1 && G <= kMaxGroups, kBadArg, "grouped_gemm: G=%d out of [1,%d]", G,
+                kMaxGroups);
+  COMOE_REQUIRE(K % 64 == 0 && K > 0, kUnsupportedShape,
+                "grouped_gemm: K=%d must be a multiple of 64", K);
+  COMOE_REQUIRE(N % 256 == 0 && N > 0, kUnsupportedShape,
+                "grouped_gemm: N=%d must be a multiple of 256", N);
+  COMOE_REQUIRE(ldo % 8 == 0, kUnsupportedShape, "grouped_gemm: ldo must be a multiple of 8");
+  COMOE_REQUIRE(a_rows > 0 && n_slots > 0, kBadArg, "grouped_gemm: empty operand");
+  COMOE_REQUIRE(b_offset % 8 == 0 && b_offset + static_cast<long>(N) * K <= slot_stride, kBadArg,
+                "grouped_gemm: B block exceeds the slot");
+  if (epi_mode == kEpiScaleScatter)
+    COMOE_REQUIRE(row_token && row_prob, kBadArg, "scatter epilogue needs row_token/row_prob");
+  CUtensorMap ta, tb;
+  int rc = make_tmap_bf16_2d(&ta, a, static_cast<uint64_t>(a_rows), K, kGemmBM);
+  if (rc) return rc;
+  const void* b = static_cast<const __nv_bfloat16*>(pool) + b_offset;
+  rc = make_tmap_bf16_3d(&tb, b, n_slots, N, K, slot_stride, 256);
+  if (rc) return rc;
+  GroupedGemmParams p{group_rows, group_row_base, group_slot, G, N, K,
+                      reinterpret_cast<__nv_bfloat16*>(out), ldo, row_token, row_prob};
+  switch (epi_mode) {
+    case kEpiRelu: return launch_gemm<256, 4, kEpiRelu>(ta, tb, p, stream);
+    case kEpiSwiGLU: return launch_gemm<256, 4, kEpiSwiGLU>(ta, tb, p, stream);
+    case kEpiScaleScatter: return launch_gemm<256, 4, kEpiScaleScatter>(ta, tb, p, stream);
+    case kEpiStore: return launch_gemm<256, 4, kEpiStore>(ta, tb, p, stream);
+    default: break;
+  }
+  set_error("grouped_gemm: unknown epilogue mode %d", epi_mode);
+  return kBadArg;
+}
+
+}  // namespace comoe
+
+extern "C" {
+
+int comoe_grouped_gemm(const void* a, long a_rows, const void* pool, int n_slots, long slot_stride,
+                       long b_offset, int N, int K, const int* group_rows,
+                       const int* group_row_base, const int* group_slot, int G, int epi_mode,
+                       void* out, int ldo, const int* row_token, const float* row_prob,
+                       void* stream) {
+  return comoe::grouped_gemm_impl(a, a_rows, pool, n_slots, slot_stride, b_offset, N, K,
+                                  group_rows, group_row_base, group_slot, G, epi_mode, out, ldo,
+                                  row_token, row_prob, static_cast<cudaStream_t>(stream));
+}
+
+int comoe_grouped_ffn(const void* x_perm, long total_rows, int d, int d_ff, int act,
+                      const void* pool, int n_slots, long slot_stride, const int* group_rows,
+                      const int* group_row_base, const int* group_slot, int G, void* h_work,
+                      void* out, int ldo, const int* row_token, const float* row_prob,
+                      void* stream) {
+  using namespace comoe;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  COMOE_REQUIRE(act == COMOE_ACT_RELU || act == COMOE_ACT_SWIGLU, kBadArg, "grouped_ffn: act=%d",
+                act);
+  COMOE_REQUIRE(h_work != nullptr, kBadArg, "grouped_ffn: null workspace");
+  const int n1 = act == COMOE_ACT_SWIGLU ? 2 * d_ff : d_ff;
+  int rc = grouped_gemm_impl(x_perm, total_rows, pool, n_slots, slot_stride, 0, n1, d, group_rows,
+                             group_row_base, group_slot, G,
+                             act == COMOE_ACT_SWIGLU ? kEpiSwiGLU : kEpiRelu, h_work, d_ff,
+                             nullptr, nullptr, s);
+  if (rc) return rc;
+  const int mode2 = row_token ? kEpiScaleScatter : kEpiStore;
+  return grouped_gemm_impl(h_work, total_rows, pool, n_slots, slot_stride,
+                           static_cast<long>(n1) * d, d, d_ff, group_rows, group_row_base,
+                           group_slot, G, mode2, out, ldo, row_token, row_prob, s);
+}
+
+}  // extern "C"

@@ -1,0 +1,453 @@
+// K1 gate + routing scan.
+//
+// The reference has no router: routing decisions come from the synthetic
+// Zipf/rho generator (pkg/src/comoe/moe.py:186-230) and are remapped to the
+// merged expert set by ModelVariant.resolve (pkg/src/comoe/aggregation.py:101-103).
+// Here the router is real: fp32 logits x.Wg on the tensor cores, softmax,
+// top-k on the logits (ties -> lowest expert index, the reference's universal
+// tie rule, aggregation.py:165,193), slot remap through the variant's
+// slot_map, and per-tile token-order ranks that feed deterministic capacity.
+//
+// fp32-faithful logits on bf16 tensor cores: X is bf16 (exact); the fp32
+// router weight is split Wg = hi + mid + lo with each term bf16, so every
+// product x*term is exact in the fp32 accumulator and the three MMAs sum to
+// the fp32 logit up to accumulation rounding.
+#include "grouped_gemm.cuh"
+#include "../../include/comoe_b200.h"
+
+namespace comoe {
+
+constexpr int kGateMaxE = 128;
+constexpr int kGateMaxK = 2;
+
+// ------------------------------------------------------------ weight split
+__global__ void gate_split_kernel(const float* __restrict__ wg, int d, int E, int EP,
+                                  __nv_bfloat16* __restrict__ out) {
+  const long n = static_cast<long>(EP) * d;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const int e = static_cast<int>(i / d), k = static_cast<int>(i % d);
+    const float w = e < E ? wg[static_cast<long>(k) * E + e] : 0.f;  // Wg is [d, E]
+    const __nv_bfloat16 hi = __float2bfloat16_rn(w);
+    const float r1 = w - __bfloat162float(hi);
+    const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+    const float r2 = r1 - __bfloat162float(mid);
+    const __nv_bfloat16 lo = __float2bfloat16_rn(r2);
+    out[i] = hi;
+    out[n + i] = mid;
+    out[2 * n + i] = lo;
+  }
+}
+
+struct GateParams {
+  int T, d, E, top_k, norm_topk, G, ntiles;
+  const int* slot_map;  // [E] -> group, may be null (identity)
+  float* logits;        // [T, E] optional
+  int* expert_idx;      // [T, k]
+  int* group_idx;       // [T, k]  (-1: no assignment)
+  float* gate_prob;     // [T, k]
+  int* local_rank;      // [T, k]
+  int* tile_hist;       // [k][ntiles][G]
+};
+
+template <int EP, int kStages>
+struct GateSmem {
+  static constexpr int kABytes = kGemmBM * kGemmBK * 2;
+  static constexpr int kBBytes = 3 * EP * kGemmBK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kTileBytes = kStages * kStageBytes;
+  static constexpr int kCtrlBytes = (2 * kStages + 4) * 8 + 16 + kGateMaxK * 4 * kGateMaxE * 4 + kGateMaxE * 4;
+  static constexpr int kTotal = 1024 + kTileBytes + kCtrlBytes;
+};
+
+template <int EP, int kStages>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gate_kernel(const __grid_constant__ CUtensorMap tmap_x,
+                const __grid_constant__ CUtensorMap tmap_w, GateParams p) {
+  using S = GateSmem<EP, kStages>;
+  constexpr uint32_t kTmemCols = 2 * EP <= 32 ? 32 : (2 * EP <= 64 ? 64 : (2 * EP <= 128 ? 128 : 256));
+  constexpr uint32_t kIdesc = umma_idesc_bf16_f32(kGemmBM, EP);
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem + kStages * S::kABytes;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S::kTileBytes);
+  uint64_t* empty_bar = full_bar + kStages;
+  uint64_t* tfull_bar = empty_bar + kStages;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  int* cnt = reinterpret_cast<int*>(tmem_slot + 4);       // [kMaxK][4][kGateMaxE]
+  int* smap = cnt + kGateMaxK * 4 * kGateMaxE;             // [kGateMaxE]
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int k_blocks = p.d / kGemmBK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_x);
+    tma_prefetch_desc(&tmap_w);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
+  for (int e = threadIdx.x; e < kGateMaxE; e += blockDim.x)
+    smap[e] = e < p.E ? (p.slot_map ? __ldg(p.slot_map + e) : e) : -1;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      const uint64_t pol_x = l2_policy_evict_first();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          mbar_expect_tx(&full_bar[stage], S::kStageBytes);
+          tma_load_2d_hint(smem_a + stage * S::kABytes, &tmap_x, &full_bar[stage], kb * kGemmBK,
+                           tile * kGemmBM, pol_x);
+          uint8_t* b = smem_b + stage * S::kBBytes;
+#pragma unroll
+          for (int term = 0; term < 3; ++term)
+            tma_load_2d(b + term * EP * 128, &tmap_w, &full_bar[stage], kb * kGemmBK, term * EP);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++it) {
+        const int acc = it & 1;
+        mbar_wait(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * EP;
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint64_t adesc = umma_desc_k_sw128(smem_u32(smem_a + stage * S::kABytes));
+#pragma unroll
+          for (int term = 0; term < 3; ++term) {
+            const uint64_t bdesc =
+                umma_desc_k_sw128(smem_u32(smem_b + stage * S::kBBytes + term * EP * 128));
+#pragma unroll
+            for (int k = 0; k < kGemmBK / 16; ++k)
+              umma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, kIdesc, (kb | k | term) != 0);
+          }
+          umma_commit(&empty_bar[stage]);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&tfull_bar[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++it) {
+      const int acc = it & 1;
+      const int t = tile * kGemmBM + q * 32 + lane;
+      const bool valid = t < p.T;
+      mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * EP;
+
+      // online softmax + running top-2 over the logits of this token
+      float m = -INFINITY, s = 0.f;
+      float v1 = -INFINITY, v2 = -INFINITY;
+      int i1 = -1, i2 = -1;
+      float* lrow = (p.logits && valid) ? p.logits + static_cast<long>(t) * p.E : nullptr;
+#pragma unroll 1
+      for (int c = 0; c < EP; c += 16) {
+        uint32_t r[16];
+        tmem_ld16(t_row + c, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int e = c + j;
+          if (e < p.E) {
+            const float v = __uint_as_float(r[j]);
+            if (lrow) lrow[e] = v;
+            if (v > m) {
+              s = s * expf(m - v) + 1.f;
+              m = v;
+            } else {
+              s += expf(v - m);
+            }
+            if (v > v1) {
+              v2 = v1; i2 = i1; v1 = v; i1 = e;
+            } else if (v > v2) {
+              v2 = v; i2 = e;
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+
+      float pr[kGateMaxK];
+      int ex[kGateMaxK], gr[kGateMaxK];
+      ex[0] = i1; ex[1] = i2;
+      if (p.top_k == 1) {
+        pr[0] = p.norm_topk ? 1.f : 1.f / s;
+        pr[1] = 0.f;
+      } else if (p.norm_topk) {
+        const float z = expf(v2 - v1);
+        pr[0] = 1.f / (1.f + z);
+        pr[1] = z / (1.f + z);
+      } else {
+        pr[0] = expf(v1 - m) / s;
+        pr[1] = expf(v2 - m) / s;
+      }
+      for (int j = 0; j < kGateMaxK; ++j)
+        gr[j] = (valid && j < p.top_k && ex[j] >= 0) ? smap[ex[j]] : -1;
+      if (p.top_k == 2 && gr[1] >= 0 && gr[1] == gr[0]) {  // both picks merged into one expert
+        pr[0] += pr[1];
+        pr[1] = 0.f;
+        gr[1] = -1;
+      }
+
+      // token-order ranks inside the tile: warp match + per-warp counts
+      named_bar_sync(1, 128);
+      for (int i = threadIdx.x - 128; i < p.top_k * 4 * kGateMaxE; i += 128) cnt[i] = 0;
+      named_bar_sync(1, 128);
+      int wrank[kGateMaxK];
+      for (int j = 0; j < p.top_k; ++j) {
+        const unsigned mask = __match_any_sync(0xffffffffu, gr[j]);
+        wrank[j] = __popc(mask & lt_mask);
+        if (gr[j] >= 0 && wrank[j] == 0) cnt[(j * 4 + q) * kGateMaxE + gr[j]] = __popc(mask);
+      }
+      named_bar_sync(1, 128);
+      if (valid) {
+        for (int j = 0; j < p.top_k; ++j) {
+          int rank = -1;
+          if (gr[j] >= 0) {
+            rank = wrank[j];
+            for (int qq = 0; qq < q; ++qq) rank += cnt[(j * 4 + qq) * kGateMaxE + gr[j]];
+          }
+          const long o = static_cast<long>(t) * p.top_k + j;
+          p.expert_idx[o] = ex[j];
+          p.group_idx[o] = gr[j];
+          p.gate_prob[o] = gr[j] >= 0 ? pr[j] : 0.f;
+          p.local_rank[o] = rank;
+        }
+      }
+      for (int j = 0; j < p.top_k; ++j)
+        for (int g = threadIdx.x - 128; g < p.G; g += 128) {
+          int h = 0;
+          if (g < kGateMaxE)
+            for (int qq = 0; qq < 4; ++qq) h += cnt[(j * 4 + qq) * kGateMaxE + g];
+          p.tile_hist[(static_cast<long>(j) * p.ntiles + tile) * p.G + g] = h;
+        }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem_base);
+  }
+}
+
+template <int EP>
+static int launch_gate(const CUtensorMap& tx, const CUtensorMap& tw, const GateParams& p,
+                       cudaStream_t stream) {
+  constexpr int kStages = EP >= 128 ? 3 : 4;
+  using S = GateSmem<EP, kStages>;
+  auto kern = gate_kernel<EP, kStages>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kTotal);
+    attr = true;
+  }
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = p.ntiles < sms ? p.ntiles : sms;
+  kern<<<grid, kGemmThreads, S::kTotal, stream>>>(tx, tw, p);
+  return check_launch("gate_kernel");
+}
+
+// ------------------------------------------------------------ routing scan
+// Column g of tile_hist in stream order (k-major, then tile): exclusive scan
+// -> tile_offset, total -> group_count.
+__global__ void route_scan_columns(const int* __restrict__ hist, int n_rows, int G,
+                                   int* __restrict__ offset, int* __restrict__ count) {
+  __shared__ int warp_tot[32];
+  const int g = blockIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int carry = 0;
+  for (int base = 0; base < n_rows; base += blockDim.x) {
+    const int r = base + threadIdx.x;
+    const int x = r < n_rows ? hist[static_cast<long>(r) * G + g] : 0;
+    int v = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int n = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += n;
+    }
+    if (lane == 31) warp_tot[w] = v;
+    __syncthreads();
+    int wb = 0, tot = 0;
+    for (int i = 0; i < nw; ++i) {
+      if (i < w) wb += warp_tot[i];
+      tot += warp_tot[i];
+    }
+    if (r < n_rows) offset[static_cast<long>(r) * G + g] = carry + wb + v - x;
+    carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) count[g] = carry;
+}
+
+// kept = min(count, C); base = exclusive scan of kept.
+__global__ void route_scan_bases(const int* __restrict__ count, int G, int capacity,
+                                 int* __restrict__ kept, int* __restrict__ base) {
+  __shared__ int warp_tot[32];
+  const int per = (G + blockDim.x - 1) / blockDim.x;
+  const int g0 = threadIdx.x * per;
+  int local = 0;
+  for (int i = 0; i < per; ++i) {
+    const int g = g0 + i;
+    if (g < G) local += min(count[g], capacity);
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int v = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int n = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += n;
+  }
+  if (lane == 31) warp_tot[w] = v;
+  __syncthreads();
+  int run = v - local;
+  for (int i = 0; i < w; ++i) run += warp_tot[i];
+  for (int i = 0; i < per; ++i) {
+    const int g = g0 + i;
+    if (g < G) {
+      const int kk = min(count[g], capacity);
+      kept[g] = kk;
+      base[g] = run;
+      run += kk;
+    }
+  }
+}
+
+__global__ void expert_hist_kernel(const int* __restrict__ idx, long n, int E,
+                                   int* __restrict__ counts) {
+  extern __shared__ int h[];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) h[e] = 0;
+  __syncthreads();
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const int e = idx[i];
+    if (e >= 0 && e < E) atomicAdd(&h[e], 1);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x)
+    if (h[e]) atomicAdd(&counts[e], h[e]);
+}
+
+}  // namespace comoe
+
+extern "C" {
+
+int comoe_gate_padded_experts(int E) {
+  if (E < 1 || E > comoe::kGateMaxE) return -1;
+  int ep = 16;
+  while (ep < E) ep <<= 1;
+  return ep;
+}
+
+int comoe_gate_prepare(const float* wg, int d, int E, void* wg_split, void* stream) {
+  using namespace comoe;
+  COMOE_REQUIRE(wg && wg_split, kBadArg, "gate_prepare: null pointer");
+  const int EP = comoe_gate_padded_experts(E);
+  COMOE_REQUIRE(EP > 0, kUnsupportedShape, "gate_prepare: E=%d must be in [1,%d]", E, kGateMaxE);
+  COMOE_REQUIRE(d > 0 && d % 64 == 0, kUnsupportedShape, "gate_prepare: d=%d must be a multiple of 64", d);
+  const long n = static_cast<long>(EP) * d;
+  const int grid = static_cast<int>((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096);
+  gate_split_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      wg, d, E, EP, reinterpret_cast<__nv_bfloat16*>(wg_split));
+  return check_launch("gate_split_kernel");
+}
+
+int comoe_gate_topk(const void* x, int T, int d, const void* wg_split, int E, int top_k,
+                    int norm_topk, const int* slot_map, int n_groups, float* logits_out,
+                    int* expert_idx, int* group_idx, float* gate_prob, int* local_rank,
+                    int* tile_hist, void* stream) {
+  using namespace comoe;
+  COMOE_REQUIRE(x && wg_split && expert_idx && group_idx && gate_prob && local_rank && tile_hist,
+                kBadArg, "gate_topk: null pointer");
+  COMOE_REQUIRE(T > 0, kBadArg, "gate_topk: T=%d", T);
+  COMOE_REQUIRE(top_k == 1 || top_k == 2, kUnsupportedShape, "gate_topk: top_k=%d not in {1,2}", top_k);
+  COMOE_REQUIRE(top_k <= E, kBadArg, "gate_topk: top_k > E");
+  const int EP = comoe_gate_padded_experts(E);
+  COMOE_REQUIRE(EP > 0, kUnsupportedShape, "gate_topk: E=%d must be in [1,%d]", E, kGateMaxE);
+  COMOE_REQUIRE(d % 64 == 0, kUnsupportedShape, "gate_topk: d=%d must be a multiple of 64", d);
+  COMOE_REQUIRE(n_groups >= 1 && n_groups <= E, kBadArg, "gate_topk: n_groups=%d", n_groups);
+  CUtensorMap tx, tw;
+  int rc = make_tmap_bf16_2d(&tx, x, T, d, kGemmBM);
+  if (rc) return rc;
+  rc = make_tmap_bf16_2d(&tw, wg_split, 3ull * EP, d, EP);
+  if (rc) return rc;
+  GateParams p{T, d, E, top_k, norm_topk, n_groups, (T + kGemmBM - 1) / kGemmBM, slot_map,
+               logits_out, expert_idx, group_idx, gate_prob, local_rank, tile_hist};
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  switch (EP) {
+    case 16: return launch_gate<16>(tx, tw, p, s);
+    case 32: return launch_gate<32>(tx, tw, p, s);
+    case 64: return launch_gate<64>(tx, tw, p, s);
+    case 128: return launch_gate<128>(tx, tw, p, s);
+    default: break;
+  }
+  set_error("gate_topk: no kernel for EP=%d", EP);
+  return kUnsupportedShape;
+}
+
+int comoe_gate_num_tiles(int T) { return (T + comoe::kGemmBM - 1) / comoe::kGemmBM; }
+
+int comoe_route_scan(const int* tile_hist, int top_k, int ntiles, int G, int capacity,
+                     int* tile_offset, int* group_count, int* group_kept, int* group_base,
+                     void* stream) {
+  using namespace comoe;
+  COMOE_REQUIRE(tile_hist && tile_offset && group_count && group_kept && group_base, kBadArg,
+                "route_scan: null pointer");
+  COMOE_REQUIRE(G >= 1 && G <= 32 * 1024, kBadArg, "route_scan: G=%d", G);
+  COMOE_REQUIRE(capacity >= 0, kBadArg, "route_scan: capacity=%d", capacity);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  route_scan_columns<<<G, 256, 0, s>>>(tile_hist, top_k * ntiles, G, tile_offset, group_count);
+  int rc = check_launch("route_scan_columns");
+  if (rc) return rc;
+  route_scan_bases<<<1, 1024, 0, s>>>(group_count, G, capacity, group_kept, group_base);
+  return check_launch("route_scan_bases");
+}
+
+int comoe_expert_histogram(const int* expert_idx, long n, int E, int* counts, void* stream) {
+  using namespace comoe;
+  COMOE_REQUIRE(expert_idx && counts && E > 0 && n >= 0, kBadArg, "expert_histogram: bad args");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaMemsetAsync(counts, 0, sizeof(int) * E, s);
+  if (n == 0) return check_launch("expert_histogram");
+  const long blocks = (n + 1023) / 1024;
+  expert_hist_kernel<<<static_cast<int>(blocks < 296 ? blocks : 296), 1024, E * sizeof(int), s>>>(
+      expert_idx, n, E, counts);
+  return check_launch("expert_hist_kernel");
+}
+
+}  // extern "C"

@@ -1,0 +1,157 @@
+// K5: CoMoE frequency-weighted expert merge, one launch per layer.
+//
+// Restates merge_group (pkg/src/comoe/aggregation.py:200-215):
+//     merged = (sum_j f_j * e_j) / sum_j f_j      (plain mean if sum f <= 1e-12)
+// for every multi-member group of a layer at once. Inputs are flat expert
+// parameter vectors (the reference's `Expert.params`, moe.py:69-74), here
+// [W_in | W_out] bf16 slots of the HBM expert pool, or fp64 vectors in the
+// parity mode. The host passes per-member weights and per-group divisors
+// (weights = f_j, divisor = sum f; or weights = 1, divisor = n for the mean).
+//
+// fp64 mode reproduces numpy's evaluation order exactly: products rounded
+// separately, rows summed in member order, one final division — no FMA
+// contraction — so results are bit-identical to the reference.
+// bf16 mode streams 16-byte vectors with fp32 accumulation (w_j/divisor
+// pre-divided in fp64), reading each member once and writing the merge once.
+#include "common.cuh"
+#include "../../include/comoe_b200.h"
+
+namespace comoe {
+
+constexpr int kMergeMaxMembers = 64;
+
+__global__ void __launch_bounds__(256) merge_bf16_kernel(const void* const* __restrict__ members,
+                                                         const int* __restrict__ offsets,
+                                                         const double* __restrict__ weights,
+                                                         const double* __restrict__ divisor,
+                                                         void* const* __restrict__ outs, long D) {
+  const int g = blockIdx.y;
+  const int m0 = offsets[g], m1 = offsets[g + 1];
+  const int n = m1 - m0;
+  __shared__ float w[kMergeMaxMembers];
+  __shared__ const int4* src[kMergeMaxMembers];
+  if (threadIdx.x < n) {
+    w[threadIdx.x] = static_cast<float>(weights[m0 + threadIdx.x] / divisor[g]);
+    src[threadIdx.x] = reinterpret_cast<const int4*>(members[m0 + threadIdx.x]);
+  }
+  __syncthreads();
+  int4* dst = reinterpret_cast<int4*>(outs[g]);
+  const long nvec = D >> 3;
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < nvec; i += stride) {
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int j = 0; j < n; ++j) {
+      const int4 raw = ld_nc_v4(src[j] + i);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+      const float wj = w[j];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float2 f = __bfloat1622float2(h[u]);
+        acc[2 * u] = fmaf(wj, f.x, acc[2 * u]);
+        acc[2 * u + 1] = fmaf(wj, f.y, acc[2 * u + 1]);
+      }
+    }
+    int4 o;
+    o.x = static_cast<int>(pack_bf16x2(acc[0], acc[1]));
+    o.y = static_cast<int>(pack_bf16x2(acc[2], acc[3]));
+    o.z = static_cast<int>(pack_bf16x2(acc[4], acc[5]));
+    o.w = static_cast<int>(pack_bf16x2(acc[6], acc[7]));
+    dst[i] = o;
+  }
+}
+
+__global__ void __launch_bounds__(256) merge_f64_kernel(const void* const* __restrict__ members,
+                                                        const int* __restrict__ offsets,
+                                                        const double* __restrict__ weights,
+                                                        const double* __restrict__ divisor,
+                                                        void* const* __restrict__ outs, long D) {
+  const int g = blockIdx.y;
+  const int m0 = offsets[g], m1 = offsets[g + 1];
+  const int n = m1 - m0;
+  __shared__ double w[kMergeMaxMembers];
+  __shared__ const double2* src[kMergeMaxMembers];
+  if (threadIdx.x < n) {
+    w[threadIdx.x] = weights[m0 + threadIdx.x];
+    src[threadIdx.x] = reinterpret_cast<const double2*>(members[m0 + threadIdx.x]);
+  }
+  __syncthreads();
+  const double div = divisor[g];
+  double2* dst = reinterpret_cast<double2*>(outs[g]);
+  const long nvec = D >> 1;
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < nvec; i += stride) {
+    const double2 v0 = src[0][i];
+    double ax = __dmul_rn(w[0], v0.x), ay = __dmul_rn(w[0], v0.y);
+    for (int j = 1; j < n; ++j) {
+      const double2 v = src[j][i];
+      ax = __dadd_rn(ax, __dmul_rn(w[j], v.x));
+      ay = __dadd_rn(ay, __dmul_rn(w[j], v.y));
+    }
+    dst[i] = make_double2(__ddiv_rn(ax, div), __ddiv_rn(ay, div));
+  }
+}
+
+__global__ void merge_f64_tail(const void* const* __restrict__ members,
+                               const int* __restrict__ offsets, const double* __restrict__ weights,
+                               const double* __restrict__ divisor, void* const* __restrict__ outs,
+                               long D) {
+  // odd D: last element per group
+  const int g = blockIdx.x;
+  if (threadIdx.x != 0) return;
+  const int m0 = offsets[g], m1 = offsets[g + 1];
+  const long i = D - 1;
+  double a = __dmul_rn(weights[m0], reinterpret_cast<const double*>(members[m0])[i]);
+  for (int j = m0 + 1; j < m1; ++j)
+    a = __dadd_rn(a, __dmul_rn(weights[j], reinterpret_cast<const double*>(members[j])[i]));
+  reinterpret_cast<double*>(outs[g])[i] = __ddiv_rn(a, divisor[g]);
+}
+
+}  // namespace comoe
+
+extern "C" {
+
+int comoe_merge(int dtype, const void* const* member_ptrs, const int* group_offsets,
+                const double* weights, const double* divisor, void* const* out_ptrs, int n_groups,
+                int max_members, long D, void* stream) {
+  using namespace comoe;
+  COMOE_REQUIRE(member_ptrs && group_offsets && weights && divisor && out_ptrs, kBadArg,
+                "merge: null pointer");
+  COMOE_REQUIRE(n_groups >= 0 && n_groups <= 65535, kBadArg, "merge: n_groups=%d", n_groups);
+  COMOE_REQUIRE(max_members >= 1 && max_members <= kMergeMaxMembers, kUnsupportedShape,
+                "merge: groups of %d members exceed %d", max_members, kMergeMaxMembers);
+  COMOE_REQUIRE(D > 0, kBadArg, "merge: D=%ld", D);
+  if (n_groups == 0) return kOk;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // ~8 resident 256-thread CTAs per SM spread over the groups of this layer
+  const long per_vec = dtype == COMOE_DTYPE_BF16 ? 8 : 2;
+  const long nvec = D / per_vec;
+  long bx = (static_cast<long>(sms) * 8 + n_groups - 1) / n_groups;
+  const long need = (nvec + 255) / 256;
+  if (bx > need) bx = need;
+  if (bx < 1) bx = 1;
+  dim3 grid(static_cast<unsigned>(bx), static_cast<unsigned>(n_groups));
+  if (dtype == COMOE_DTYPE_BF16) {
+    COMOE_REQUIRE(D % 8 == 0, kUnsupportedShape, "merge(bf16): D=%ld must be a multiple of 8", D);
+    merge_bf16_kernel<<<grid, 256, 0, s>>>(member_ptrs, group_offsets, weights, divisor, out_ptrs, D);
+    return check_launch("merge_bf16_kernel");
+  }
+  if (dtype == COMOE_DTYPE_F64) {
+    if (nvec > 0) {
+      merge_f64_kernel<<<grid, 256, 0, s>>>(member_ptrs, group_offsets, weights, divisor, out_ptrs, D);
+      int rc = check_launch("merge_f64_kernel");
+      if (rc) return rc;
+    }
+    if (D & 1) {
+      merge_f64_tail<<<n_groups, 32, 0, s>>>(member_ptrs, group_offsets, weights, divisor, out_ptrs, D);
+      return check_launch("merge_f64_tail");
+    }
+    return kOk;
+  }
+  set_error("merge: unsupported dtype %d", dtype);
+  return kBadArg;
+}
+
+}  // extern "C"

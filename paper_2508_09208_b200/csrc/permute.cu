@@ -1,0 +1,170 @@
+// K2 permute (scatter-by-expert with capacity) and K4 combine (unpermute).
+//
+// Neither exists in the reference (its "forward" is the analytic charge at
+// pkg/src/comoe/simulator.py:692-707); the semantics are the Switch/GShard
+// ones written down in DESIGN.md: an assignment (token t, choice j) of group g
+// has rank = tokens before it in stream order (all first choices in token
+// order, then all second choices); it is kept iff rank < capacity and lands
+// at row base[g] + rank of the compact, expert-sorted buffer.
+#include "common.cuh"
+#include "../../include/comoe_b200.h"
+
+namespace comoe {
+
+struct PermuteParams {
+  const __nv_bfloat16* x;
+  int T, d, top_k, G, capacity, ntiles;
+  const int* group_idx;
+  const float* gate_prob;
+  const int* local_rank;
+  const int* tile_offset;
+  const int* group_base;
+  __nv_bfloat16* x_perm;
+  int* row_token;
+  float* row_prob;
+  int* token_pos;      // [T, k] destination row or -1
+  __nv_bfloat16* y;    // optional: zero rows of fully-dropped tokens (top-1 fused combine)
+};
+
+constexpr int kRowUnroll = 4;
+
+// One warp per token: rank -> destination, then a vectorised row copy per kept choice.
+__global__ void __launch_bounds__(256) permute_kernel(PermuteParams p) {
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int vec = p.d >> 3;  // uint4 per row
+  for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < p.T; t += warps) {
+    const int tile = t / 128;
+    int dest[2] = {-1, -1};
+    for (int j = 0; j < p.top_k; ++j) {
+      const long o = static_cast<long>(t) * p.top_k + j;
+      const int g = __ldg(p.group_idx + o);
+      if (g >= 0) {
+        const int rank = __ldg(p.tile_offset + (static_cast<long>(j) * p.ntiles + tile) * p.G + g) +
+                         __ldg(p.local_rank + o);
+        if (rank < p.capacity) dest[j] = __ldg(p.group_base + g) + rank;
+      }
+      if (lane == 0) {
+        p.token_pos[o] = dest[j];
+        if (dest[j] >= 0) {
+          p.row_token[dest[j]] = t;
+          p.row_prob[dest[j]] = __ldg(p.gate_prob + o);
+        }
+      }
+    }
+    const int4* src = reinterpret_cast<const int4*>(p.x + static_cast<long>(t) * p.d);
+    const bool any = dest[0] >= 0 || dest[1] >= 0;
+    if (any) {
+      int4* d0 = dest[0] >= 0 ? reinterpret_cast<int4*>(p.x_perm + static_cast<long>(dest[0]) * p.d) : nullptr;
+      int4* d1 = dest[1] >= 0 ? reinterpret_cast<int4*>(p.x_perm + static_cast<long>(dest[1]) * p.d) : nullptr;
+      for (int i0 = 0; i0 < vec; i0 += 32 * kRowUnroll) {
+        int4 v[kRowUnroll];
+#pragma unroll
+        for (int u = 0; u < kRowUnroll; ++u) {
+          const int i = i0 + u * 32 + lane;
+          if (i < vec) v[u] = ld_nc_v4(src + i);
+        }
+#pragma unroll
+        for (int u = 0; u < kRowUnroll; ++u) {
+          const int i = i0 + u * 32 + lane;
+          if (i < vec) {
+            if (d0) d0[i] = v[u];
+            if (d1) d1[i] = v[u];
+          }
+        }
+      }
+    } else if (p.y) {
+      int4* yr = reinterpret_cast<int4*>(p.y + static_cast<long>(t) * p.d);
+      const int4 z = make_int4(0, 0, 0, 0);
+      for (int i = lane; i < vec; i += 32) yr[i] = z;
+    }
+  }
+}
+
+// y[t] = sum_j prob_j * y_perm[pos_j]  (pos -1 contributes 0), fp32 accumulate.
+__global__ void __launch_bounds__(256) combine_kernel(const __nv_bfloat16* __restrict__ y_perm,
+                                                      const int* __restrict__ token_pos,
+                                                      const float* __restrict__ gate_prob, int T,
+                                                      int d, int top_k,
+                                                      __nv_bfloat16* __restrict__ y) {
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int vec = d >> 3;
+  for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < T; t += warps) {
+    int pos[2] = {-1, -1};
+    float pr[2] = {0.f, 0.f};
+    for (int j = 0; j < top_k; ++j) {
+      pos[j] = __ldg(token_pos + static_cast<long>(t) * top_k + j);
+      pr[j] = __ldg(gate_prob + static_cast<long>(t) * top_k + j);
+    }
+    int4* dst = reinterpret_cast<int4*>(y + static_cast<long>(t) * d);
+    for (int i = lane; i < vec; i += 32) {
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      for (int j = 0; j < top_k; ++j) {
+        if (pos[j] < 0) continue;
+        const int4 raw = ld_nc_v4(reinterpret_cast<const int4*>(y_perm + static_cast<long>(pos[j]) * d) + i);
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float2 f = __bfloat1622float2(h[u]);
+          acc[2 * u] = fmaf(pr[j], f.x, acc[2 * u]);
+          acc[2 * u + 1] = fmaf(pr[j], f.y, acc[2 * u + 1]);
+        }
+      }
+      int4 out;
+      out.x = static_cast<int>(pack_bf16x2(acc[0], acc[1]));
+      out.y = static_cast<int>(pack_bf16x2(acc[2], acc[3]));
+      out.z = static_cast<int>(pack_bf16x2(acc[4], acc[5]));
+      out.w = static_cast<int>(pack_bf16x2(acc[6], acc[7]));
+      dst[i] = out;
+    }
+  }
+}
+
+static int grid_for_warps(long warps_needed) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long blocks = (warps_needed + 7) / 8;
+  const long cap = static_cast<long>(sms) * 8;  // 8 x 256-thread CTAs per SM
+  return static_cast<int>(blocks < cap ? (blocks > 0 ? blocks : 1) : cap);
+}
+
+}  // namespace comoe
+
+extern "C" {
+
+int comoe_permute(const void* x, int T, int d, int top_k, const int* group_idx,
+                  const float* gate_prob, const int* local_rank, const int* tile_offset,
+                  const int* group_base, int n_groups, int capacity, void* x_perm,
+                  int* row_token, float* row_prob, int* token_pos, void* y_zero, void* stream) {
+  using namespace comoe;
+  COMOE_REQUIRE(x && group_idx && gate_prob && local_rank && tile_offset && group_base && x_perm &&
+                    row_token && row_prob && token_pos,
+                kBadArg, "permute: null pointer");
+  COMOE_REQUIRE(top_k == 1 || top_k == 2, kUnsupportedShape, "permute: top_k=%d", top_k);
+  COMOE_REQUIRE(d % 8 == 0 && d > 0, kUnsupportedShape, "permute: d=%d must be a multiple of 8", d);
+  COMOE_REQUIRE(T >= 0 && n_groups >= 1, kBadArg, "permute: bad sizes");
+  if (T == 0) return kOk;
+  PermuteParams p{reinterpret_cast<const __nv_bfloat16*>(x), T, d, top_k, n_groups, capacity,
+                  (T + 127) / 128, group_idx, gate_prob, local_rank, tile_offset, group_base,
+                  reinterpret_cast<__nv_bfloat16*>(x_perm), row_token, row_prob, token_pos,
+                  reinterpret_cast<__nv_bfloat16*>(y_zero)};
+  permute_kernel<<<grid_for_warps(T), 256, 0, static_cast<cudaStream_t>(stream)>>>(p);
+  return check_launch("permute_kernel");
+}
+
+int comoe_combine(const void* y_perm, const int* token_pos, const float* gate_prob, int T, int d,
+                  int top_k, void* y, void* stream) {
+  using namespace comoe;
+  COMOE_REQUIRE(y_perm && token_pos && gate_prob && y, kBadArg, "combine: null pointer");
+  COMOE_REQUIRE(top_k == 1 || top_k == 2, kUnsupportedShape, "combine: top_k=%d", top_k);
+  COMOE_REQUIRE(d % 8 == 0 && d > 0, kUnsupportedShape, "combine: d=%d", d);
+  if (T == 0) return kOk;
+  combine_kernel<<<grid_for_warps(T), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const __nv_bfloat16*>(y_perm), token_pos, gate_prob, T, d, top_k,
+      reinterpret_cast<__nv_bfloat16*>(y));
+  return check_launch("combine_kernel");
+}
+
+}  // extern "C"

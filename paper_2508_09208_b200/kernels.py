@@ -1,0 +1,332 @@
+"""Thin PyTorch-facing wrappers over the C ABI (one function per kernel).
+
+PyTorch only provides device memory and the current stream here; every
+computation below runs in libcomoe_b200.so. Arguments are validated on the
+host (device, dtype, contiguity, alignment) before the C call, which
+validates sizes again and reports through comoe_last_error().
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+
+ACT_RELU, ACT_SWIGLU = 0, 1
+EPI_RELU, EPI_SWIGLU, EPI_SCALE_SCATTER, EPI_STORE = 0, 1, 2, 3
+DTYPE_BF16, DTYPE_F64 = 0, 1
+GEMM_BM = 128
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _need(t: torch.Tensor, name: str, dtype=None, dims=None):
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must live on a CUDA device (no CPU path)")
+    if dtype is not None and t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if dims is not None and t.dim() != dims:
+        raise ValueError(f"{name} must be {dims}-D, got shape {tuple(t.shape)}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if t.data_ptr() % 16:
+        raise ValueError(f"{name} must be 16-byte aligned")
+    return t
+
+
+def num_sms(device=None) -> int:
+    dev = torch.cuda.current_device() if device is None else device
+    return _lib.load().comoe_num_sms(int(dev))
+
+
+# ---------------------------------------------------------------- K1 gate
+
+def gate_padded_experts(E: int) -> int:
+    ep = _lib.load().comoe_gate_padded_experts(int(E))
+    if ep < 0:
+        raise ValueError(f"gate supports 1..128 experts, got {E}")
+    return ep
+
+
+def gate_num_tiles(T: int) -> int:
+    return (int(T) + GEMM_BM - 1) // GEMM_BM
+
+
+def gate_prepare(wg: torch.Tensor) -> torch.Tensor:
+    """fp32 router Wg[d, E] -> bf16 split terms [3, EP, d] (hi, mid, lo)."""
+    _need(wg, "wg", torch.float32, 2)
+    d, E = wg.shape
+    ep = gate_padded_experts(E)
+    out = torch.empty((3, ep, d), dtype=torch.bfloat16, device=wg.device)
+    _lib.call("comoe_gate_prepare", _ptr(wg), d, E, _ptr(out), _stream())
+    return out
+
+
+@dataclass
+class GateOutput:
+    expert_idx: torch.Tensor   # [T, k] int32 original expert
+    group_idx: torch.Tensor    # [T, k] int32 group after slot remap, -1 = none
+    gate_prob: torch.Tensor    # [T, k] float32
+    local_rank: torch.Tensor   # [T, k] int32 rank inside the 128-token tile
+    tile_hist: torch.Tensor    # [k, ntiles, G] int32
+    logits: torch.Tensor = None  # [T, E] float32 (optional)
+
+
+def gate_topk(x, wg_split, E, top_k, norm_topk, slot_map=None, n_groups=None,
+              want_logits=False, out: GateOutput = None) -> GateOutput:
+    _need(x, "x", torch.bfloat16, 2)
+    _need(wg_split, "wg_split", torch.bfloat16, 3)
+    T, d = x.shape
+    G = E if n_groups is None else int(n_groups)
+    if slot_map is not None:
+        _need(slot_map, "slot_map", torch.int32, 1)
+    nt = gate_num_tiles(T)
+    dev = x.device
+    if out is None:
+        out = GateOutput(
+            expert_idx=torch.empty((T, top_k), dtype=torch.int32, device=dev),
+            group_idx=torch.empty((T, top_k), dtype=torch.int32, device=dev),
+            gate_prob=torch.empty((T, top_k), dtype=torch.float32, device=dev),
+            local_rank=torch.empty((T, top_k), dtype=torch.int32, device=dev),
+            tile_hist=torch.empty((top_k, nt, G), dtype=torch.int32, device=dev),
+            logits=torch.empty((T, E), dtype=torch.float32, device=dev) if want_logits else None)
+    _lib.call("comoe_gate_topk", _ptr(x), T, d, _ptr(wg_split), E, top_k, int(norm_topk),
+              _ptr(slot_map), G, _ptr(out.logits), _ptr(out.expert_idx), _ptr(out.group_idx),
+              _ptr(out.gate_prob), _ptr(out.local_rank), _ptr(out.tile_hist), _stream())
+    return out
+
+
+@dataclass
+class ScanOutput:
+    tile_offset: torch.Tensor  # [k, ntiles, G]
+    group_count: torch.Tensor  # [G] assignments before capacity
+    group_kept: torch.Tensor   # [G]
+    group_base: torch.Tensor   # [G]
+
+
+def route_scan(tile_hist, capacity: int, out: ScanOutput = None) -> ScanOutput:
+    _need(tile_hist, "tile_hist", torch.int32, 3)
+    k, nt, G = tile_hist.shape
+    dev = tile_hist.device
+    if out is None:
+        out = ScanOutput(torch.empty_like(tile_hist),
+                         *(torch.empty(G, dtype=torch.int32, device=dev) for _ in range(3)))
+    _lib.call("comoe_route_scan", _ptr(tile_hist), k, nt, G, int(capacity), _ptr(out.tile_offset),
+              _ptr(out.group_count), _ptr(out.group_kept), _ptr(out.group_base), _stream())
+    return out
+
+
+def expert_histogram(expert_idx: torch.Tensor, E: int, out=None) -> torch.Tensor:
+    _need(expert_idx, "expert_idx", torch.int32)
+    if out is None:
+        out = torch.empty(E, dtype=torch.int32, device=expert_idx.device)
+    _lib.call("comoe_expert_histogram", _ptr(expert_idx), expert_idx.numel(), E, _ptr(out),
+              _stream())
+    return out
+
+
+# ---------------------------------------------------------------- K2 / K4
+
+@dataclass
+class PermuteOutput:
+    x_perm: torch.Tensor     # [rows, d] bf16
+    row_token: torch.Tensor  # [rows] int32
+    row_prob: torch.Tensor   # [rows] float32
+    token_pos: torch.Tensor  # [T, k] int32
+
+
+def permute(x, gate: GateOutput, scan: ScanOutput, capacity: int, rows: int,
+            y_zero=None, out: PermuteOutput = None) -> PermuteOutput:
+    _need(x, "x", torch.bfloat16, 2)
+    T, d = x.shape
+    k = gate.group_idx.shape[1]
+    G = scan.group_base.numel()
+    dev = x.device
+    if out is None:
+        out = PermuteOutput(torch.empty((max(rows, 1), d), dtype=torch.bfloat16, device=dev),
+                            torch.empty(max(rows, 1), dtype=torch.int32, device=dev),
+                            torch.empty(max(rows, 1), dtype=torch.float32, device=dev),
+                            torch.empty((T, k), dtype=torch.int32, device=dev))
+    if y_zero is not None:
+        _need(y_zero, "y_zero", torch.bfloat16, 2)
+    _lib.call("comoe_permute", _ptr(x), T, d, k, _ptr(gate.group_idx), _ptr(gate.gate_prob),
+              _ptr(gate.local_rank), _ptr(scan.tile_offset), _ptr(scan.group_base), G,
+              int(capacity), _ptr(out.x_perm), _ptr(out.row_token), _ptr(out.row_prob),
+              _ptr(out.token_pos), _ptr(y_zero), _stream())
+    return out
+
+
+def combine(y_perm, token_pos, gate_prob, out=None) -> torch.Tensor:
+    _need(y_perm, "y_perm", torch.bfloat16, 2)
+    _need(token_pos, "token_pos", torch.int32, 2)
+    _need(gate_prob, "gate_prob", torch.float32, 2)
+    T, k = token_pos.shape
+    d = y_perm.shape[1]
+    if out is None:
+        out = torch.empty((T, d), dtype=torch.bfloat16, device=y_perm.device)
+    _lib.call("comoe_combine", _ptr(y_perm), _ptr(token_pos), _ptr(gate_prob), T, d, k,
+              _ptr(out), _stream())
+    return out
+
+
+# ---------------------------------------------------------------- K3
+
+def expert_numel(d: int, d_ff: int, act: int) -> int:
+    n1 = 2 * d_ff if act == ACT_SWIGLU else d_ff
+    return n1 * d + d * d_ff
+
+
+def grouped_ffn(x_perm, pool, d_ff, act, group_rows, group_row_base, group_slot, h_work, out,
+                row_token=None, row_prob=None):
+    _need(x_perm, "x_perm", torch.bfloat16, 2)
+    _need(pool, "pool", torch.bfloat16, 2)
+    _need(h_work, "h_work", torch.bfloat16, 2)
+    _need(out, "out", torch.bfloat16, 2)
+    for name, t in (("group_rows", group_rows), ("group_row_base", group_row_base),
+                    ("group_slot", group_slot)):
+        _need(t, name, torch.int32, 1)
+    rows, d = x_perm.shape
+    if h_work.shape[0] < rows or h_work.shape[1] != d_ff:
+        raise ValueError("h_work must be [rows, d_ff]")
+    if pool.shape[1] < expert_numel(d, d_ff, act):
+        raise ValueError("pool slot too small for the expert shape")
+    _lib.call("comoe_grouped_ffn", _ptr(x_perm), rows, d, d_ff, act, _ptr(pool), pool.shape[0],
+              pool.shape[1], _ptr(group_rows), _ptr(group_row_base), _ptr(group_slot),
+              group_rows.numel(), _ptr(h_work), _ptr(out), out.shape[1], _ptr(row_token),
+              _ptr(row_prob), _stream())
+    return out
+
+
+def grouped_gemm(a, pool, b_offset, N, group_rows, group_row_base, group_slot, epi_mode, out,
+                 row_token=None, row_prob=None):
+    _need(a, "a", torch.bfloat16, 2)
+    _need(pool, "pool", torch.bfloat16, 2)
+    _need(out, "out", torch.bfloat16, 2)
+    rows, K = a.shape
+    _lib.call("comoe_grouped_gemm", _ptr(a), rows, _ptr(pool), pool.shape[0], pool.shape[1],
+              int(b_offset), int(N), K, _ptr(group_rows), _ptr(group_row_base),
+              _ptr(group_slot), group_rows.numel(), int(epi_mode), _ptr(out), out.shape[1],
+              _ptr(row_token), _ptr(row_prob), _stream())
+    return out
+
+
+# ---------------------------------------------------------------- K5 merge
+
+def merge_groups(groups_members, weights, divisors, outs, dtype) -> None:
+    """groups_members: list (per group) of member tensors (flat, same numel);
+    weights: list of per-member float weights; divisors: per-group float;
+    outs: per-group output tensors. One launch for all groups."""
+    if not groups_members:
+        return
+    dev = outs[0].device
+    D = outs[0].numel()
+    code = DTYPE_BF16 if dtype == torch.bfloat16 else DTYPE_F64
+    if dtype not in (torch.bfloat16, torch.float64):
+        raise ValueError("merge supports bf16 and float64 parameters")
+    ptrs, offs, ws = [], [0], []
+    for members, wlist in zip(groups_members, weights):
+        if len(members) != len(wlist):
+            raise ValueError("one weight per member")
+        for m in members:
+            _need(m, "member", dtype)
+            if m.numel() != D:
+                raise ValueError("member size mismatch")
+            ptrs.append(m.data_ptr())
+        ws.extend(float(w) for w in wlist)
+        offs.append(len(ptrs))
+    for o in outs:
+        _need(o, "out", dtype)
+        if o.numel() != D:
+            raise ValueError("output size mismatch")
+    max_members = max(offs[i + 1] - offs[i] for i in range(len(outs)))
+    t_ptrs = torch.tensor(ptrs, dtype=torch.int64).to(dev, non_blocking=False)
+    t_offs = torch.tensor(offs, dtype=torch.int32).to(dev)
+    t_w = torch.tensor(ws, dtype=torch.float64).to(dev)
+    t_div = torch.tensor([float(x) for x in divisors], dtype=torch.float64).to(dev)
+    t_out = torch.tensor([o.data_ptr() for o in outs], dtype=torch.int64).to(dev)
+    _lib.call("comoe_merge", code, _ptr(t_ptrs), _ptr(t_offs), _ptr(t_w), _ptr(t_div),
+              _ptr(t_out), len(outs), max_members, D, _stream())
+    # the caching allocator is stream-ordered, so the pointer tables may be
+    # released now: any reuse is enqueued after this kernel on the same stream
+    del t_ptrs, t_offs, t_w, t_div, t_out
+
+
+# ---------------------------------------------------------------- K6 similarity
+
+def similarity(rows, probes, proj, alpha):
+    """rows: list of E flat expert tensors (bf16 or float64, same numel);
+    probes [n, D], proj [B, D] float64 on the device. Returns (S, gram,
+    logits) float64 device tensors."""
+    E = len(rows)
+    D = rows[0].numel()
+    dt = rows[0].dtype
+    if dt not in (torch.bfloat16, torch.float64):
+        raise ValueError("similarity supports bf16 and float64 parameters")
+    for r in rows:
+        _need(r, "row", dt)
+        if r.numel() != D:
+            raise ValueError("parameter dimension mismatch")
+    _need(probes, "probes", torch.float64, 2)
+    _need(proj, "proj", torch.float64, 2)
+    n, B = probes.shape[0], proj.shape[0]
+    if probes.shape[1] != D or proj.shape[1] != D:
+        raise ValueError("calibration dimension mismatch")
+    dev = rows[0].device
+    t_rows = torch.tensor([r.data_ptr() for r in rows], dtype=torch.int64).to(dev)
+    ws = _lib.load().comoe_sim_workspace_bytes(E, n, B, D)
+    work = torch.empty(max(ws, 8), dtype=torch.uint8, device=dev)
+    gram = torch.empty((E, E), dtype=torch.float64, device=dev)
+    logits = torch.empty((E, n, B), dtype=torch.float64, device=dev)
+    sim = torch.empty((E, E), dtype=torch.float64, device=dev)
+    code = DTYPE_BF16 if dt == torch.bfloat16 else DTYPE_F64
+    _lib.call("comoe_sim_contract", code, _ptr(t_rows), E, D, _ptr(probes), n, _ptr(proj), B,
+              _ptr(gram), _ptr(logits), _ptr(work), _stream())
+    _lib.call("comoe_sim_finalize", _ptr(gram), _ptr(logits), E, n, B, float(alpha), _ptr(sim),
+              _stream())
+    return sim, gram, logits
+
+
+# ---------------------------------------------------------------- K8 predictor
+
+def predictor_mlp(slots, emb, ctx, w1, b1, w2, b2, want_demand=False):
+    _need(slots, "slots", torch.int32, 2)
+    B, K = slots.shape
+    for name, t in (("w1", w1), ("b1", b1), ("w2", w2), ("b2", b2)):
+        _need(t, name, torch.float64)
+    E, hidden = w2.shape
+    emb_dim = 0 if emb is None else emb.shape[1]
+    ctx_dim = 0 if ctx is None else ctx.shape[1]
+    if emb is not None:
+        _need(emb, "emb", torch.float64, 2)
+    if ctx is not None:
+        _need(ctx, "ctx", torch.float64, 2)
+    if w1.shape[1] != E + emb_dim + ctx_dim:
+        raise ValueError("embedding/context dims do not match the predictor")
+    probs = torch.empty((B, E), dtype=torch.float64, device=slots.device)
+    demand = torch.empty(E, dtype=torch.float64, device=slots.device) if want_demand else None
+    _lib.call("comoe_predictor_mlp", _ptr(slots), B, K, _ptr(emb), emb_dim, _ptr(ctx), ctx_dim,
+              _ptr(w1), _ptr(b1), hidden, _ptr(w2), _ptr(b2), E, _ptr(probs), _ptr(demand),
+              _stream())
+    return (probs, demand) if want_demand else probs
+
+
+def capacity_for(T: int, n_groups: int, top_k: int, capacity_factor) -> int:
+    """C = ceil(cf * T * k / G) (GShard/Switch); None -> no drops."""
+    if capacity_factor is None:
+        return int(T) * int(top_k)
+    return int(math.ceil(float(capacity_factor) * int(T) * int(top_k) / int(n_groups)))

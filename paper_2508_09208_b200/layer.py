@@ -1,0 +1,168 @@
+"""MoELayer: the B200 MoE-layer forward (the new `MoELayer.forward(x)` of
+SURVEY §8b). Replaces the reference's per-token analytic layer charge
+(pkg/src/comoe/simulator.py:684-724, expert compute at :705) with
+
+    K1 gate (tcgen05 fp32-faithful logits, softmax, top-k, slot remap, tile ranks)
+    -> route scan (capacity in stream order, group bases)
+    -> K2 permute (expert-sorted compact rows; zero rows of dropped tokens)
+    -> K3 grouped FFN (tcgen05 GEMM1 + act -> H, GEMM2 -> fused top-1 combine)
+    -> K4 combine (top-2 only)
+
+all enqueued on the current stream, no host synchronisation. Expert weights
+live in an ExpertPool; a merged variant only changes the slot_map LUT and
+the per-group slot list, never the kernels.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import kernels
+from .pool import ExpertPool
+
+ACTS = {"relu": kernels.ACT_RELU, "swiglu": kernels.ACT_SWIGLU}
+
+
+@dataclass
+class LayerRouting:
+    gate: kernels.GateOutput
+    scan: kernels.ScanOutput
+    perm: kernels.PermuteOutput
+    capacity: int
+    rows: int
+
+
+class MoELayer:
+    def __init__(self, wg: torch.Tensor, pool: ExpertPool, d_ff: int, act: str = "relu",
+                 top_k: int = 1, norm_topk: bool = None, capacity_factor=1.25,
+                 expert_slots=None):
+        if act not in ACTS:
+            raise ValueError(f"act must be one of {sorted(ACTS)}")
+        if top_k not in (1, 2):
+            raise ValueError("top_k must be 1 or 2")
+        kernels._need(wg, "wg", torch.float32, 2)
+        self.d, self.E = wg.shape
+        self.d_ff = int(d_ff)
+        self.act = act
+        self.top_k = top_k
+        self.norm_topk = (top_k > 1) if norm_topk is None else bool(norm_topk)
+        self.capacity_factor = capacity_factor
+        self.pool = pool
+        if pool.numel < kernels.expert_numel(self.d, self.d_ff, ACTS[act]):
+            raise ValueError("pool slots are too small for this expert shape")
+        self.wg = wg
+        self.wg_split = kernels.gate_prepare(wg)
+        slots = list(range(self.E)) if expert_slots is None else list(expert_slots)
+        self.set_variant(list(range(self.E)), slots)
+        self._ws = {}
+        self.last: LayerRouting = None
+
+    # ------------------------------------------------------------ variants
+    def set_variant(self, slot_map, group_slots) -> None:
+        """slot_map[E]: original expert -> group index; group_slots[G]: pool
+        slot serving each group (ModelVariant.group_table gives both)."""
+        slot_map = [int(s) for s in slot_map]
+        group_slots = [int(s) for s in group_slots]
+        G = len(group_slots)
+        if len(slot_map) != self.E or any(not 0 <= g < G for g in slot_map):
+            raise ValueError("slot_map must map every expert to a group index")
+        if any(not 0 <= s < self.pool.n_slots for s in group_slots):
+            raise ValueError("group slot outside the pool")
+        dev = self.wg.device
+        self.G = G
+        self.slot_map = torch.tensor(slot_map, dtype=torch.int32, device=dev)
+        self.group_slot = torch.tensor(group_slots, dtype=torch.int32, device=dev)
+        self._ws = {}
+
+    def use_variant(self, variant, layer: int) -> None:
+        """Point the layer at a ModelVariant whose retained experts live in
+        this layer's pool (aggregation.fuse_model(..., pool=...))."""
+        lut, principals = variant.group_table(layer, self.E)
+        slots = []
+        for p in principals:
+            s = self.pool.slot_of(variant.retained[layer][p].params)
+            if s is None:
+                raise ValueError(f"expert ({layer},{p}) is not a slot of this layer's pool")
+            slots.append(s)
+        self.set_variant(lut, slots)
+
+    # ------------------------------------------------------------ workspace
+    def capacity(self, T: int) -> int:
+        return kernels.capacity_for(T, self.G, self.top_k, self.capacity_factor)
+
+    def _workspace(self, T: int):
+        ws = self._ws.get(T)
+        if ws is not None:
+            return ws
+        dev = self.wg.device
+        C = self.capacity(T)
+        rows = max(1, min(T * self.top_k, self.G * C))
+        k, nt = self.top_k, kernels.gate_num_tiles(T)
+        ws = dict(
+            C=C, rows=rows,
+            gate=kernels.GateOutput(
+                torch.empty((T, k), dtype=torch.int32, device=dev),
+                torch.empty((T, k), dtype=torch.int32, device=dev),
+                torch.empty((T, k), dtype=torch.float32, device=dev),
+                torch.empty((T, k), dtype=torch.int32, device=dev),
+                torch.empty((k, nt, self.G), dtype=torch.int32, device=dev)),
+            scan=kernels.ScanOutput(torch.empty((k, nt, self.G), dtype=torch.int32, device=dev),
+                                    *(torch.empty(self.G, dtype=torch.int32, device=dev)
+                                      for _ in range(3))),
+            perm=kernels.PermuteOutput(torch.empty((rows, self.d), dtype=torch.bfloat16, device=dev),
+                                       torch.empty(rows, dtype=torch.int32, device=dev),
+                                       torch.empty(rows, dtype=torch.float32, device=dev),
+                                       torch.empty((T, k), dtype=torch.int32, device=dev)),
+            h=torch.empty((rows, self.d_ff), dtype=torch.bfloat16, device=dev),
+            y_perm=torch.empty((rows, self.d), dtype=torch.bfloat16, device=dev) if k > 1 else None,
+        )
+        self._ws[T] = ws
+        return ws
+
+    # ------------------------------------------------------------ forward
+    def route(self, x: torch.Tensor, want_logits: bool = False) -> LayerRouting:
+        kernels._need(x, "x", torch.bfloat16, 2)
+        T = x.shape[0]
+        ws = self._workspace(T)
+        gate = ws["gate"]
+        if want_logits:
+            gate = kernels.GateOutput(gate.expert_idx, gate.group_idx, gate.gate_prob,
+                                      gate.local_rank, gate.tile_hist,
+                                      torch.empty((T, self.E), dtype=torch.float32, device=x.device))
+        kernels.gate_topk(x, self.wg_split, self.E, self.top_k, self.norm_topk,
+                          slot_map=self.slot_map, n_groups=self.G, out=gate)
+        kernels.route_scan(gate.tile_hist, ws["C"], out=ws["scan"])
+        return LayerRouting(gate, ws["scan"], ws["perm"], ws["C"], ws["rows"])
+
+    def forward(self, x: torch.Tensor, out: torch.Tensor = None,
+                want_logits: bool = False) -> torch.Tensor:
+        if x.shape[1] != self.d:
+            raise ValueError(f"x must be [T, {self.d}]")
+        T = x.shape[0]
+        if out is None:
+            out = torch.empty((T, self.d), dtype=torch.bfloat16, device=x.device)
+        if T == 0:
+            return out
+        ws = self._workspace(T)
+        r = self.route(x, want_logits)
+        k1 = self.top_k == 1
+        kernels.permute(x, r.gate, r.scan, r.capacity, r.rows, y_zero=out if k1 else None,
+                        out=r.perm)
+        dst = out if k1 else ws["y_perm"]
+        kernels.grouped_ffn(r.perm.x_perm, self.pool.data, self.d_ff, ACTS[self.act],
+                            r.scan.group_kept, r.scan.group_base, self.group_slot, ws["h"], dst,
+                            row_token=r.perm.row_token if k1 else None,
+                            row_prob=r.perm.row_prob if k1 else None)
+        if not k1:
+            kernels.combine(ws["y_perm"], r.perm.token_pos, r.gate.gate_prob, out=out)
+        self.last = r
+        return out
+
+    __call__ = forward
+
+    @property
+    def kernels_per_forward(self) -> int:
+        """Device kernels one forward launches (gate, 2x scan, permute, 2x GEMM [, combine])."""
+        return 6 + (0 if self.top_k == 1 else 1)

@@ -1,0 +1,139 @@
+"""Device merge (K5), similarity (K6) and predictor (K8) against the oracle
+and against reference-generated golden vectors."""
+
+import hashlib
+import json
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import GOLDEN
+from oracle import merge as M
+
+pytestmark = pytest.mark.gpu
+
+
+def _experts(P, dtype=torch.float64):
+    from paper_2508_09208_b200.moe import Expert
+    return [Expert(1, s, torch.as_tensor(np.asarray(p), dtype=dtype, device="cuda"), 1.0)
+            for s, p in enumerate(P)]
+
+
+def _stats(counts):
+    from paper_2508_09208_b200.moe import ActivationStats
+    c = np.asarray(counts, float)
+    return ActivationStats(counts={1: c}, totals={1: max(int(c.sum()), 1)}, experts_per_layer=len(c))
+
+
+def test_merge_hand_cases():
+    from paper_2508_09208_b200.aggregation import ExpertGroup, merge_group
+    for case in json.loads((GOLDEN / "merge_hand.json").read_text()):
+        ex = _experts(case["vectors"])
+        f = np.asarray(case["freqs"])
+        counts = f * 4 if f.sum() > 0 else f
+        st = _stats(counts)
+        if f.sum() == 0:
+            st.totals[1] = 10
+        m = merge_group(ExpertGroup(0, (1,)), {0: ex[0], 1: ex[1]}, st, 1)
+        np.testing.assert_array_equal(m.params.cpu().numpy(), np.asarray(case["expected"]))
+
+
+def test_merge_f64_bit_exact_vs_reference_checksums():
+    from paper_2508_09208_b200 import kernels
+    for case in json.loads((GOLDEN / "merge_bigsum.json").read_text()):
+        rng = np.random.default_rng(case["seed"])
+        V = rng.normal(size=(case["n"], case["D"])) * 0.02
+        f = np.asarray(case["counts"])
+        Vd = torch.as_tensor(V, device="cuda")
+        out = torch.empty(case["D"], dtype=torch.float64, device="cuda")
+        if f.sum() > 0:
+            w, div = list(f), float(f.sum())
+        else:
+            w, div = [1.0] * case["n"], float(case["n"])
+        kernels.merge_groups([[Vd[i] for i in range(case["n"])]], [w], [div], [out], torch.float64)
+        got = out.cpu().numpy()
+        assert hashlib.sha256(got.tobytes()).hexdigest() == case["sha256"]
+
+
+def test_merge_bf16_tolerance_sb8_shape():
+    """Switch expert size (D = 4,718,592), groups of 2/4/8 members: every
+    element within 1 bf16 ulp of bf16(fp64 merge) + 2^-24 max|input|."""
+    from paper_2508_09208_b200 import kernels
+    from oracle.switch_layer import bf16_round
+    D = 4_718_592
+    g = torch.Generator(device="cuda").manual_seed(2)
+    V = (torch.randn(8, D, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+    for n in (2, 4, 8):
+        f = np.arange(1, n + 1, dtype=float)
+        out = torch.empty(D, dtype=torch.bfloat16, device="cuda")
+        kernels.merge_groups([[V[i] for i in range(n)]], [list(f)], [float(f.sum())], [out],
+                             torch.bfloat16)
+        Vh = V[:n].double().cpu().numpy()
+        ref = M.merge_params(list(Vh), f)
+        refb = bf16_round(ref.astype(np.float32)).astype(np.float64)
+        got = out.double().cpu().numpy()
+        ulp = np.abs(refb) * 2.0 ** -7
+        bound = ulp + 2.0 ** -24 * np.abs(Vh).max()
+        assert np.all(np.abs(got - refb) <= bound + 1e-30)
+
+
+def test_fusion_pipeline_matches_reference_golden():
+    """fuse_model on the device reproduces the reference's decisions
+    (principals, groups, slot_map) and merged params to rel 1e-9, with the
+    reference's own similarity matrix checked to 1e-9 as well."""
+    from paper_2508_09208_b200 import aggregation as A
+    from paper_2508_09208_b200.moe import Calibration, MoeModel, MoeModelSpec, similarity_matrix
+    for case in json.loads((GOLDEN / "fusion_cases.json").read_text()):
+        E = case["E"]
+        P = np.asarray(case["params"])
+        ex = _experts(P)
+        calib = Calibration(np.asarray(case["probes"]), np.asarray(case["projection"]))
+        S = similarity_matrix(ex, case["alpha"], calib)
+        np.testing.assert_allclose(S, np.asarray(case["sim"]), rtol=1e-9, atol=1e-9)
+        spec = MoeModelSpec(2, (1,), (), E, 1e6, 1, case["dim"])
+        model = MoeModel(spec, {(1, e.slot): e for e in ex})
+        st = _stats(case["counts"])
+        cfg = A.FusionConfig(mode="fixed", r=case["r"], theta_act=case["theta_act"])
+        var = A.fuse_model(model, st, cfg, case["alpha"], calib)
+        assert {str(k): v for k, v in var.slot_map[1].items()} == case["slot_map"]
+        assert sorted(var.retained[1]) == case["principals"]
+        for p, ref in case["merged"].items():
+            np.testing.assert_allclose(var.retained[1][int(p)].params.cpu().numpy(),
+                                       np.asarray(ref), rtol=1e-9, atol=1e-12)
+        assert var.perf_estimate == pytest.approx(case["perf_estimate"], rel=1e-9)
+
+
+def test_similarity_bf16_switch_scale():
+    """K6 on bf16 Switch-size experts (E=8, D=4.7M) vs fp64 oracle of the
+    same bf16 values (sigma 0.02 keeps the reference surrogate finite)."""
+    from paper_2508_09208_b200.moe import Expert, make_calibration, similarity_matrix
+    D, E = 4_718_592, 8
+    g = torch.Generator(device="cuda").manual_seed(5)
+    V = (torch.randn(E, D, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+    calib = make_calibration(D, n_probes=8, seed=7, buckets=8)
+    S = similarity_matrix([Expert(1, s, V[s], 1.0) for s in range(E)], 0.5, calib)
+    ref = M.similarity(V.double().cpu().numpy(), calib.probes, calib.projection, 0.5)
+    np.testing.assert_allclose(S, ref, rtol=1e-7, atol=1e-7)
+
+
+def test_predictor_matches_numpy():
+    from paper_2508_09208_b200 import kernels
+    rng = np.random.default_rng(0)
+    E, emb, ctx, H, B, K = 128, 16, 8, 32, 1000, 1
+    w1 = rng.normal(scale=0.1, size=(H, E + emb + ctx)); b1 = rng.normal(size=H) * 0.1
+    w2 = rng.normal(scale=0.1, size=(E, H)); b2 = rng.normal(size=E) * 0.1
+    slots = rng.integers(0, E, size=(B, K)).astype(np.int32)
+    he = rng.normal(size=(B, emb)); ce = rng.normal(size=(B, ctx))
+    X = np.zeros((B, E + emb + ctx))
+    X[np.arange(B), slots[:, 0]] = 1.0
+    X[:, E:E + emb] = he
+    X[:, E + emb:] = ce
+    z = np.maximum(X @ w1.T + b1, 0) @ w2.T + b2
+    z -= z.max(1, keepdims=True)
+    ref = np.exp(z) / np.exp(z).sum(1, keepdims=True)
+    d = lambda a: torch.as_tensor(a, device="cuda")
+    probs, demand = kernels.predictor_mlp(d(slots), d(he), d(ce), d(w1), d(b1), d(w2), d(b2),
+                                          want_demand=True)
+    np.testing.assert_allclose(probs.cpu().numpy(), ref, rtol=1e-10, atol=1e-13)
+    np.testing.assert_allclose(demand.cpu().numpy(), ref.sum(0), rtol=1e-10)

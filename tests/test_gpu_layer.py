@@ -1,0 +1,182 @@
+"""Device parity of the MoE-layer hot path against the CPU oracle.
+
+Routing (indices, group remap, tile ranks, histograms, capacity scan,
+permutation order) must be bit-exact given the device's fp32 logits; logits
+within fp32 accumulation error of the fp64 oracle; layer outputs within the
+bf16 normwise tolerance below.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import switch_layer as O
+
+pytestmark = pytest.mark.gpu
+
+NORMWISE_TOL = 5e-3       # bf16 storage of H and Y
+LOGIT_ABS_TOL = 2e-5      # fp32-faithful split router vs fp64 oracle, |logit| ~ 1..5
+PROB_TOL = 2e-6
+
+
+def _layer_inputs(T, d, d_ff, E, act, seed=0, dev="cuda"):
+    from paper_2508_09208_b200 import kernels
+    g = torch.Generator().manual_seed(seed)
+    x = torch.randn(T, d, generator=g).to(torch.bfloat16)
+    wg = torch.randn(d, E, generator=g) / math.sqrt(d)
+    numel = kernels.expert_numel(d, d_ff, kernels.ACT_SWIGLU if act == "swiglu" else kernels.ACT_RELU)
+    w = (torch.randn(E, numel, generator=g) * 0.02).to(torch.bfloat16)
+    return x.to(dev), wg.to(dev), w
+
+
+def _build(T, d, d_ff, E, act, top_k, cf, seed=0):
+    from paper_2508_09208_b200 import ExpertPool, MoELayer
+    x, wg, w = _layer_inputs(T, d, d_ff, E, act, seed)
+    pool = ExpertPool(E, w.shape[1])
+    for s in range(E):
+        pool.view(s).copy_(w[s].cuda())
+    layer = MoELayer(wg, pool, d_ff, act=act, top_k=top_k, capacity_factor=cf)
+    return layer, x, wg, w
+
+
+def _np(t):
+    return t.detach().float().cpu().numpy() if t.dtype == torch.bfloat16 else t.detach().cpu().numpy()
+
+
+def _check_routing(layer, x, wg, info, T):
+    r = layer.last
+    g = r.gate
+    # logits vs fp64 oracle
+    ref_logits = O.gate_logits(_np(x), _np(wg)).astype(np.float64)
+    got_logits = g.logits.cpu().numpy().astype(np.float64)
+    assert np.max(np.abs(got_logits - ref_logits)) < LOGIT_ABS_TOL
+    # bit-exact routing given identical logits
+    np.testing.assert_array_equal(g.expert_idx.cpu().numpy(), info["expert_idx"])
+    np.testing.assert_array_equal(g.group_idx.cpu().numpy(), info["group_idx"])
+    gp = g.gate_prob.cpu().numpy().astype(np.float64)
+    assert np.max(np.abs(gp - info["prob"])) < PROB_TOL
+    np.testing.assert_array_equal(g.local_rank.cpu().numpy(), info["local_rank"])
+    np.testing.assert_array_equal(g.tile_hist.cpu().numpy(), info["tile_hist"])
+    s = r.scan
+    np.testing.assert_array_equal(s.group_count.cpu().numpy(), info["count"])
+    np.testing.assert_array_equal(s.group_kept.cpu().numpy(), info["kept"])
+    np.testing.assert_array_equal(s.group_base.cpu().numpy(), info["base"])
+    np.testing.assert_array_equal(r.perm.token_pos.cpu().numpy(), info["pos"])
+    rows = int(info["kept"].sum())
+    np.testing.assert_array_equal(r.perm.row_token[:rows].cpu().numpy(), info["row_token"])
+    # the permuted rows are exact copies of the token rows
+    xp = r.perm.x_perm[:rows].cpu()
+    assert torch.equal(xp, x.cpu()[torch.as_tensor(info["row_token"])])
+
+
+@pytest.mark.parametrize("T,d,d_ff,E,cf", [
+    (1000, 256, 512, 8, 1.25),      # ragged last tile
+    (4096, 256, 512, 16, 1.0),      # drops
+    (2048, 768, 3072, 8, 1.25),     # Switch FFN shape (sb8 slice)
+    (3000, 256, 256, 128, 1.25),    # E = 128 gate
+    (777, 512, 1024, 32, None),     # no capacity limit
+])
+def test_switch_layer_top1(T, d, d_ff, E, cf):
+    layer, x, wg, w = _build(T, d, d_ff, E, "relu", 1, cf)
+    y = layer.forward(x, want_logits=True)
+    torch.cuda.synchronize()
+    logits = layer.last.gate.logits.cpu().numpy()
+    ref, info = O.layer_forward(_np(x), _np(wg), [_np(w[e]) for e in range(E)], top_k=1,
+                                capacity_factor=cf, act="relu", d_ff=d_ff, logits=logits)
+    _check_routing(layer, x, wg, info, T)
+    err = O.normwise_error(_np(y), ref)
+    assert err < NORMWISE_TOL, err
+    dropped = (info["pos"][:, 0] < 0)
+    if dropped.any():
+        assert torch.all(y[torch.as_tensor(np.nonzero(dropped)[0]).cuda()] == 0)
+
+
+@pytest.mark.parametrize("T,d,d_ff,E,norm", [
+    (1024, 256, 512, 8, True),     # Mixtral semantics (renormalised top-2)
+    (1500, 256, 256, 8, False),
+])
+def test_swiglu_layer_top2(T, d, d_ff, E, norm):
+    from paper_2508_09208_b200 import ExpertPool, MoELayer
+    x, wg, w = _layer_inputs(T, d, d_ff, E, "swiglu", seed=3)
+    pool = ExpertPool(E, w.shape[1])
+    pool.data[:, : w.shape[1]].copy_(w.cuda())
+    layer = MoELayer(wg, pool, d_ff, act="swiglu", top_k=2, norm_topk=norm, capacity_factor=1.25)
+    y = layer.forward(x, want_logits=True)
+    torch.cuda.synchronize()
+    logits = layer.last.gate.logits.cpu().numpy()
+    ref, info = O.layer_forward(_np(x), _np(wg), [_np(w[e]) for e in range(E)], top_k=2,
+                                norm_topk=norm, capacity_factor=1.25, act="swiglu", d_ff=d_ff,
+                                logits=logits)
+    _check_routing(layer, x, wg, info, T)
+    assert O.normwise_error(_np(y), ref) < NORMWISE_TOL
+
+
+def test_merged_variant_routing_and_output():
+    """8 experts merged into 4 groups: slot remap in the gate, capacity on
+    the merged count, FFN on merged pool slots."""
+    T, d, d_ff, E = 2048, 256, 512, 8
+    layer, x, wg, w = _build(T, d, d_ff, E, "relu", 1, 1.25)
+    slot_map = [0, 1, 2, 3, 0, 1, 2, 3]
+    merged = torch.stack([(w[g].float() + w[g + 4].float()) * 0.5 for g in range(4)]).to(torch.bfloat16)
+    for g in range(4):
+        layer.pool.view(g).copy_(merged[g].cuda())
+    layer.set_variant(slot_map, [0, 1, 2, 3])
+    y = layer.forward(x, want_logits=True)
+    torch.cuda.synchronize()
+    logits = layer.last.gate.logits.cpu().numpy()
+    ref, info = O.layer_forward(_np(x), _np(wg), [_np(merged[g]) for g in range(4)], top_k=1,
+                                capacity_factor=1.25, slot_map=slot_map, act="relu", d_ff=d_ff,
+                                logits=logits)
+    _check_routing(layer, x, wg, info, T)
+    assert O.normwise_error(_np(y), ref) < NORMWISE_TOL
+
+
+def test_forward_is_deterministic():
+    layer, x, wg, w = _build(4096, 256, 512, 16, "relu", 1, 1.0)
+    y1 = layer.forward(x).clone()
+    r1 = layer.last.perm.row_token.clone()
+    y2 = layer.forward(x)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2)
+    assert torch.equal(r1, layer.last.perm.row_token)
+
+
+def test_full_size_properties_sb128():
+    """C2 shape (T=65536, E=128, cf=1.25): size-independent properties."""
+    T, d, d_ff, E = 65536, 768, 3072, 128
+    from paper_2508_09208_b200 import ExpertPool, MoELayer
+    torch.manual_seed(0)
+    x = torch.randn(T, d, device="cuda").to(torch.bfloat16)
+    wg = torch.randn(d, E, device="cuda") / math.sqrt(d)
+    pool = ExpertPool(E, 2 * d * d_ff)
+    pool.data.normal_(0, 0.02)
+    layer = MoELayer(wg, pool, d_ff, capacity_factor=1.25)
+    y = layer.forward(x, want_logits=True)
+    torch.cuda.synchronize()
+    r = layer.last
+    assert r.capacity == 640
+    count = r.scan.group_count.cpu().numpy()
+    kept = r.scan.group_kept.cpu().numpy()
+    assert count.sum() == T
+    np.testing.assert_array_equal(kept, np.minimum(count, 640))
+    pos = r.perm.token_pos.cpu().numpy()[:, 0]
+    assert (pos >= 0).sum() == kept.sum()
+    # permutation is a bijection onto [0, kept.sum())
+    assert np.array_equal(np.sort(pos[pos >= 0]), np.arange(kept.sum()))
+    # routing equals the oracle's on the device logits (vectorised check)
+    logits = r.gate.logits.cpu().numpy()
+    idx, grp, prob = O.topk_route(logits, 1, False)
+    np.testing.assert_array_equal(r.gate.expert_idx.cpu().numpy(), idx)
+    # spot-check 256 tokens of the output against the oracle expert FFN
+    rng = np.random.default_rng(0)
+    toks = rng.choice(np.nonzero(pos >= 0)[0], 256, replace=False)
+    xs = x[torch.as_tensor(toks).cuda()].float().cpu().numpy()
+    ref = np.zeros((len(toks), d))
+    for i, t in enumerate(toks):
+        e = int(idx[t, 0])
+        w_in, w_out = O.split_expert(pool.view(e).float().cpu().numpy(), d, d_ff, "relu")
+        ref[i] = prob[t, 0] * O.expert_ffn(xs[i:i + 1], w_in, w_out, "relu")[0]
+    assert O.normwise_error(y[torch.as_tensor(toks).cuda()].float().cpu().numpy(), ref) < NORMWISE_TOL
+    assert torch.all(y[torch.as_tensor(np.nonzero(pos < 0)[0]).cuda()] == 0)
