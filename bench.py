@@ -1,0 +1,332 @@
+"""Benchmark of the CoMoE MoE-layer hot path on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload = BASELINE.json configs[1] (C2): Switch-Base-128-shaped MoE layer
+(d_model 768, d_ff 3072, 128 experts, top-1, capacity factor 1.25), 65,536
+synthetic tokens per GPU, all experts HBM-resident, random-init weights.
+A step = one layer forward (gate -> scan -> permute -> grouped FFN with the
+fused combine) over one batch. N>1 (torchrun) = expert parallelism with NCCL
+all-to-all dispatch/combine, 65,536 tokens per GPU (weak scaling).
+
+`--impl reference` times the reference CPU path of this layer on the host
+cores (the oracle port, oracle/switch_layer.layer_forward_fast: the
+reference itself has no tensor forward) on a bounded token sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "MoE-layer tokens/sec (Switch-Base-128 shape) + % roofline at 1/2/4/8 B200"
+UNIT = "tokens/s"
+T_PER_GPU, D, D_FF, E, TOP_K, CF = 65536, 768, 3072, 128, 1, 1.25
+CPU_SAMPLE_TOKENS = 16384
+L2_BYTES = 126 * 2 ** 20
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def _config(n):
+    return {"workload": "C2: Switch-Base-128 MoE layer forward, 65536 tokens/GPU, all experts "
+                        "HBM-resident",
+            "d_model": D, "d_ff": D_FF, "experts": E, "top_k": TOP_K, "capacity_factor": CF,
+            "tokens_per_gpu": T_PER_GPU, "global_batch_tokens": T_PER_GPU * n,
+            "parallelism": "single GPU" if n == 1 else f"ep{n} (NCCL all-to-all)",
+            "l2": "no flush: per-step inputs (x 100.7 MB + expert weights 1208 MB) exceed the "
+                  "126 MB L2"}
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), parts[2:]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, flags in rows for i, f in enumerate(flags)
+                          if f.lower().startswith("active")})
+        load = [r for r in rows if r[0] > 0.5 * r[1]] or rows
+        sm = sorted(r[0] for r in load)
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": rows[0][1], "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ---------------------------------------------------------------- CPU arm
+def cpu_layer_sample(tokens: int, seed: int = 0, reps: int = 3):
+    """Time the CPU path (oracle port, NumPy fp32 BLAS) on `tokens` tokens of
+    the C2 layer; returns (tokens/s, seconds, threads)."""
+    import numpy as np
+    from oracle import switch_layer as O
+    threads = len(os.sched_getaffinity(0))
+    rng = np.random.default_rng(seed)
+    x = O.bf16_round(rng.standard_normal((tokens, D), dtype=np.float32))
+    wg = (rng.standard_normal((D, E), dtype=np.float32) / math.sqrt(D)).astype(np.float32)
+    w_in = O.bf16_round(rng.standard_normal((E, D_FF, D), dtype=np.float32) * 0.02)
+    w_out = O.bf16_round(rng.standard_normal((E, D, D_FF), dtype=np.float32) * 0.02)
+    O.layer_forward_fast(x[:1024], wg, w_in, w_out, TOP_K, False, CF)  # warm-up
+    best = float("inf")
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        O.layer_forward_fast(x, wg, w_in, w_out, TOP_K, False, CF)
+        best = min(best, time.perf_counter() - t0)
+    return tokens / best, best, threads
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return  # N>1: rank 0 alone measures the host-CPU reference arm
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(len(os.sched_getaffinity(0))))
+    import numpy as np
+    from oracle import switch_layer as O
+    threads = len(os.sched_getaffinity(0))
+    rng = np.random.default_rng(0)
+    tok = 4096  # one bounded sample per step
+    x = O.bf16_round(rng.standard_normal((tok, D), dtype=np.float32))
+    wg = (rng.standard_normal((D, E), dtype=np.float32) / math.sqrt(D)).astype(np.float32)
+    w_in = O.bf16_round(rng.standard_normal((E, D_FF, D), dtype=np.float32) * 0.02)
+    w_out = O.bf16_round(rng.standard_normal((E, D, D_FF), dtype=np.float32) * 0.02)
+    for _ in range(args.warmup):
+        O.layer_forward_fast(x, wg, w_in, w_out, TOP_K, False, CF)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.layer_forward_fast(x, wg, w_in, w_out, TOP_K, False, CF)
+    dt = time.perf_counter() - t0
+    value = tok * args.steps / dt
+    sample = (f"{tok} tokens per step of the C2 layer (E=128, cf 1.25 -> C=40), NumPy fp32 BLAS "
+              f"oracle port of the layer forward, {threads} host threads")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": _config(args.gpus),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ---------------------------------------------------------------- GPU arm
+def _profile_summary():
+    p = ROOT / "profiles" / "latest_ffn1_traffic.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text())
+        except ValueError:
+            return None
+    return None
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2508_09208_b200 import ExpertPool, MoELayer
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if \
+        (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    bf16_peak = peaks.get("bf16_tflops", 1590.0)
+    peak_src = "measured burst (MEASURED_PEAKS.json)" if peaks else "fallback (B200_PROFILING.md)"
+
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    x = torch.randn(T_PER_GPU, D, device=dev, generator=g).to(torch.bfloat16)
+    wg = torch.randn(D, E, device=dev, generator=torch.Generator(device=dev).manual_seed(1)) / math.sqrt(D)
+    if world > 1:
+        from paper_2508_09208_b200.ep import EPMoELayer
+        layer = EPMoELayer.synthetic(wg, D_FF, E, world, rank, capacity_factor=CF, seed=2)
+    else:
+        pool = ExpertPool(E, 2 * D * D_FF, device=dev)
+        pool.data.normal_(0.0, 0.02, generator=torch.Generator(device=dev).manual_seed(2))
+        layer = MoELayer(wg, pool, D_FF, act="relu", top_k=TOP_K, capacity_factor=CF)
+    y = torch.empty_like(x)
+    stream = torch.cuda.current_stream()
+
+    stage_ev = {}
+
+    class _Stage:
+        def __init__(self, name):
+            self.name = name
+
+        def __enter__(self):
+            a = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            self.a = a
+            return self
+
+        def __exit__(self, *exc):
+            b = torch.cuda.Event(enable_timing=True)
+            b.record(stream)
+            stage_ev.setdefault(self.name, []).append((self.a, b))
+            return False
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        layer.forward(x, out=y)
+    barrier()
+
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        start.record(stream)
+        for _ in range(args.steps):
+            layer.forward(x, out=y, timer=_Stage)
+        end.record(stream)
+        barrier()
+    ms = start.elapsed_time(end) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    stages = {k: sum(a.elapsed_time(b) for a, b in v) / len(v) for k, v in stage_ev.items()}
+
+    # tokens processed: every token passes the gate and the combine; report kept ratio too
+    kept = int(layer.last.scan.group_kept.sum().item()) if hasattr(layer, "last") and layer.last else None
+    value = T_PER_GPU * world / (ms * 1e-3)
+
+    # dominant kernel roofline: grouped GEMM (ffn1/ffn2) on the tensor pipe
+    dom = max(("ffn1", "ffn2"), key=lambda k: stages.get(k, 0.0))
+    rows = kept if kept is not None else T_PER_GPU
+    flops = 2.0 * rows * D * D_FF
+    achieved = flops / (stages[dom] * 1e-3) / 1e12
+    prof = _profile_summary() or {}
+    roofline = {"bound": "tensor", "kernel": f"grouped_gemm ({dom})", "achieved": achieved,
+                "peak": bf16_peak, "unit": "TFLOP/s", "frac": achieved / bf16_peak,
+                "peak_source": peak_src,
+                "algorithmic": f"2*kept_rows*d*d_ff = {flops:.4g} FLOP per launch (kept_rows={rows})",
+                "traffic": prof.get(f"{dom}_dram_bytes_per_launch")}
+
+    # ------------------------------------------------ end-to-end (host buffers)
+    e2e = None
+    if not args.no_e2e:
+        xh = x.cpu().pin_memory()
+        yh = torch.empty_like(xh).pin_memory()
+        xd = torch.empty_like(x)
+        for _ in range(2):
+            xd.copy_(xh, non_blocking=True)
+            layer.forward(xd, out=y)
+            yh.copy_(y, non_blocking=True)
+        barrier()
+        s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s2.record(stream)
+        for _ in range(args.steps):
+            xd.copy_(xh, non_blocking=True)
+            layer.forward(xd, out=y)
+            yh.copy_(y, non_blocking=True)
+        e2.record(stream)
+        barrier()
+        ms_e2e = s2.elapsed_time(e2) / args.steps
+        if world > 1:
+            t = torch.tensor([ms_e2e], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_e2e = float(t.item())
+        nbytes = xh.numel() * xh.element_size()
+        e2e = {"value": T_PER_GPU * world / (ms_e2e * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+               "ms_per_step": ms_e2e,
+               "path": "pinned host x -> H2D -> MoELayer.forward -> D2H y, one stream"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        os.environ.setdefault("OPENBLAS_NUM_THREADS", str(len(os.sched_getaffinity(0))))
+        v, secs, threads = cpu_layer_sample(CPU_SAMPLE_TOKENS)
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"{CPU_SAMPLE_TOKENS} tokens of the C2 layer (cf 1.25 -> C=160), "
+                         f"NumPy fp32 BLAS oracle port, best of 3 ({secs:.2f} s each)"}
+
+    launches = getattr(layer, "kernels_per_forward", 6) * args.steps
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (x~N(0,1) bf16, Wg~N(0,1/d) fp32, experts~N(0,0.02^2) bf16)",
+            "config": _config(world), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clk.summary(),
+            "stages_ms": stages, "kept_rows": kept,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = _args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

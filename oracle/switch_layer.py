@@ -213,3 +213,67 @@ def normwise_error(got, ref) -> float:
     ref = np.asarray(ref, np.float64)
     den = np.linalg.norm(ref)
     return float(np.linalg.norm(got - ref) / (den if den > 0 else 1.0))
+
+
+# ---------------------------------------------------------------------------
+# vectorised CPU path (the timed CPU baseline; same semantics as above)
+
+
+def dispatch_fast(group, n_groups: int, cap: int):
+    """Vectorised `dispatch` (ranks by a stable sort in stream order)."""
+    group = np.asarray(group, np.int64)
+    T, k = group.shape
+    flat = group.T.reshape(-1)            # stream order: choice-major, then token
+    valid = flat >= 0
+    order = np.argsort(np.where(valid, flat, n_groups), kind="stable")
+    sorted_g = np.where(valid, flat, n_groups)[order]
+    count_all = np.bincount(sorted_g, minlength=n_groups + 1)
+    count = count_all[:n_groups]
+    starts = np.concatenate([[0], np.cumsum(count_all)[:-1]])
+    rank_sorted = np.arange(flat.size) - starts[sorted_g]
+    rank_flat = np.empty(flat.size, np.int64)
+    rank_flat[order] = rank_sorted
+    rank_flat[~valid] = -1
+    kept = np.minimum(count, cap)
+    base = np.concatenate([[0], np.cumsum(kept)[:-1]]).astype(np.int64)
+    keep = valid & (rank_flat < cap)
+    pos_flat = np.full(flat.size, -1, np.int64)
+    pos_flat[keep] = base[flat[keep]] + rank_flat[keep]
+    pos = pos_flat.reshape(k, T).T.copy()
+    rank = rank_flat.reshape(k, T).T.copy()
+    row_token = np.full(int(kept.sum()), -1, np.int64)
+    tok = np.tile(np.arange(T), k)
+    row_token[pos_flat[keep]] = tok[keep]
+    return dict(rank=rank, count=count, kept=kept, base=base, pos=pos, row_token=row_token)
+
+
+def layer_forward_fast(x, wg, w_in, w_out, top_k=1, norm_topk=False, capacity_factor=1.25,
+                       slot_map=None, act="relu", dtype=np.float32):
+    """CPU forward with NumPy BLAS: x [T,d], wg [d,E], w_in [G,N1,d],
+    w_out [G,d,d_ff] (already `dtype`). Returns y [T,d] (dtype)."""
+    x = np.asarray(x, dtype)
+    logits = (x @ np.asarray(wg, dtype)).astype(np.float32)
+    idx, group, prob = topk_route(logits, top_k, norm_topk, slot_map)
+    G = w_in.shape[0]
+    cap = capacity(x.shape[0], G, top_k, capacity_factor)
+    disp = dispatch_fast(group, G, cap)
+    y = np.zeros_like(x)
+    rows = np.zeros((len(disp["row_token"]), x.shape[1]), dtype)
+    for g in range(G):
+        lo, n = int(disp["base"][g]), int(disp["kept"][g])
+        if n == 0:
+            continue
+        xs = x[disp["row_token"][lo:lo + n]]
+        a = xs @ w_in[g].T
+        if act == "relu":
+            h = np.maximum(a, 0)
+        else:
+            n1 = a.shape[1]
+            b = a.reshape(n, n1 // (2 * SWIGLU_BLOCK), 2, SWIGLU_BLOCK)
+            h = (b[:, :, 0] / (1 + np.exp(-b[:, :, 0])) * b[:, :, 1]).reshape(n, n1 // 2)
+        rows[lo:lo + n] = h @ w_out[g].T
+    for j in range(top_k):
+        p = disp["pos"][:, j]
+        m = p >= 0
+        y[m] += prob[m, j][:, None].astype(dtype) * rows[p[m]]
+    return y, dict(expert_idx=idx, group_idx=group, prob=prob, capacity=cap, **disp)

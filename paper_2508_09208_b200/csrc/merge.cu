@@ -69,41 +69,21 @@ __global__ void __launch_bounds__(256) merge_f64_kernel(const void* const* __res
   const int m0 = offsets[g], m1 = offsets[g + 1];
   const int n = m1 - m0;
   __shared__ double w[kMergeMaxMembers];
-  __shared__ const double2* src[kMergeMaxMembers];
+  __shared__ const double* src[kMergeMaxMembers];
   if (threadIdx.x < n) {
     w[threadIdx.x] = weights[m0 + threadIdx.x];
-    src[threadIdx.x] = reinterpret_cast<const double2*>(members[m0 + threadIdx.x]);
+    src[threadIdx.x] = reinterpret_cast<const double*>(members[m0 + threadIdx.x]);
   }
   __syncthreads();
   const double div = divisor[g];
-  double2* dst = reinterpret_cast<double2*>(outs[g]);
-  const long nvec = D >> 1;
+  double* dst = reinterpret_cast<double*>(outs[g]);
   const long stride = static_cast<long>(gridDim.x) * blockDim.x;
-  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < nvec; i += stride) {
-    const double2 v0 = src[0][i];
-    double ax = __dmul_rn(w[0], v0.x), ay = __dmul_rn(w[0], v0.y);
-    for (int j = 1; j < n; ++j) {
-      const double2 v = src[j][i];
-      ax = __dadd_rn(ax, __dmul_rn(w[j], v.x));
-      ay = __dadd_rn(ay, __dmul_rn(w[j], v.y));
-    }
-    dst[i] = make_double2(__ddiv_rn(ax, div), __ddiv_rn(ay, div));
+  // scalar, 8-byte aligned rows (parity mode: odd D and row views allowed)
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < D; i += stride) {
+    double a = __dmul_rn(w[0], src[0][i]);
+    for (int j = 1; j < n; ++j) a = __dadd_rn(a, __dmul_rn(w[j], src[j][i]));
+    dst[i] = __ddiv_rn(a, div);
   }
-}
-
-__global__ void merge_f64_tail(const void* const* __restrict__ members,
-                               const int* __restrict__ offsets, const double* __restrict__ weights,
-                               const double* __restrict__ divisor, void* const* __restrict__ outs,
-                               long D) {
-  // odd D: last element per group
-  const int g = blockIdx.x;
-  if (threadIdx.x != 0) return;
-  const int m0 = offsets[g], m1 = offsets[g + 1];
-  const long i = D - 1;
-  double a = __dmul_rn(weights[m0], reinterpret_cast<const double*>(members[m0])[i]);
-  for (int j = m0 + 1; j < m1; ++j)
-    a = __dadd_rn(a, __dmul_rn(weights[j], reinterpret_cast<const double*>(members[j])[i]));
-  reinterpret_cast<double*>(outs[g])[i] = __ddiv_rn(a, divisor[g]);
 }
 
 }  // namespace comoe
@@ -126,7 +106,7 @@ int comoe_merge(int dtype, const void* const* member_ptrs, const int* group_offs
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // ~8 resident 256-thread CTAs per SM spread over the groups of this layer
-  const long per_vec = dtype == COMOE_DTYPE_BF16 ? 8 : 2;
+  const long per_vec = dtype == COMOE_DTYPE_BF16 ? 8 : 1;
   const long nvec = D / per_vec;
   long bx = (static_cast<long>(sms) * 8 + n_groups - 1) / n_groups;
   const long need = (nvec + 255) / 256;
@@ -139,16 +119,8 @@ int comoe_merge(int dtype, const void* const* member_ptrs, const int* group_offs
     return check_launch("merge_bf16_kernel");
   }
   if (dtype == COMOE_DTYPE_F64) {
-    if (nvec > 0) {
-      merge_f64_kernel<<<grid, 256, 0, s>>>(member_ptrs, group_offsets, weights, divisor, out_ptrs, D);
-      int rc = check_launch("merge_f64_kernel");
-      if (rc) return rc;
-    }
-    if (D & 1) {
-      merge_f64_tail<<<n_groups, 32, 0, s>>>(member_ptrs, group_offsets, weights, divisor, out_ptrs, D);
-      return check_launch("merge_f64_tail");
-    }
-    return kOk;
+    merge_f64_kernel<<<grid, 256, 0, s>>>(member_ptrs, group_offsets, weights, divisor, out_ptrs, D);
+    return check_launch("merge_f64_kernel");
   }
   set_error("merge: unsupported dtype %d", dtype);
   return kBadArg;

@@ -33,7 +33,7 @@ def _stream(stream=None):
     return ctypes.c_void_p(s.cuda_stream)
 
 
-def _need(t: torch.Tensor, name: str, dtype=None, dims=None):
+def _need(t: torch.Tensor, name: str, dtype=None, dims=None, align=16):
     if not isinstance(t, torch.Tensor):
         raise TypeError(f"{name} must be a torch.Tensor")
     if not t.is_cuda:
@@ -44,8 +44,8 @@ def _need(t: torch.Tensor, name: str, dtype=None, dims=None):
         raise ValueError(f"{name} must be {dims}-D, got shape {tuple(t.shape)}")
     if not t.is_contiguous():
         raise ValueError(f"{name} must be contiguous")
-    if t.data_ptr() % 16:
-        raise ValueError(f"{name} must be 16-byte aligned")
+    if t.data_ptr() % align:
+        raise ValueError(f"{name} must be {align}-byte aligned")
     return t
 
 
@@ -243,14 +243,14 @@ def merge_groups(groups_members, weights, divisors, outs, dtype) -> None:
         if len(members) != len(wlist):
             raise ValueError("one weight per member")
         for m in members:
-            _need(m, "member", dtype)
+            _need(m, "member", dtype, align=16 if dtype == torch.bfloat16 else 8)
             if m.numel() != D:
                 raise ValueError("member size mismatch")
             ptrs.append(m.data_ptr())
         ws.extend(float(w) for w in wlist)
         offs.append(len(ptrs))
     for o in outs:
-        _need(o, "out", dtype)
+        _need(o, "out", dtype, align=16 if dtype == torch.bfloat16 else 8)
         if o.numel() != D:
             raise ValueError("output size mismatch")
     max_members = max(offs[i + 1] - offs[i] for i in range(len(outs)))
@@ -278,7 +278,7 @@ def similarity(rows, probes, proj, alpha):
     if dt not in (torch.bfloat16, torch.float64):
         raise ValueError("similarity supports bf16 and float64 parameters")
     for r in rows:
-        _need(r, "row", dt)
+        _need(r, "row", dt, align=r.element_size())
         if r.numel() != D:
             raise ValueError("parameter dimension mismatch")
     _need(probes, "probes", torch.float64, 2)

@@ -25,6 +25,18 @@ from .pool import ExpertPool
 ACTS = {"relu": kernels.ACT_RELU, "swiglu": kernels.ACT_SWIGLU}
 
 
+class _NoTimer:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
+def _no_timer(name):
+    return _NoTimer()
+
+
 @dataclass
 class LayerRouting:
     gate: kernels.GateOutput
@@ -137,7 +149,9 @@ class MoELayer:
         return LayerRouting(gate, ws["scan"], ws["perm"], ws["C"], ws["rows"])
 
     def forward(self, x: torch.Tensor, out: torch.Tensor = None,
-                want_logits: bool = False) -> torch.Tensor:
+                want_logits: bool = False, timer=None) -> torch.Tensor:
+        """`timer`: optional callable(name) -> context manager recording
+        CUDA events around each stage on the current stream (bench.py)."""
         if x.shape[1] != self.d:
             raise ValueError(f"x must be [T, {self.d}]")
         T = x.shape[0]
@@ -146,17 +160,29 @@ class MoELayer:
         if T == 0:
             return out
         ws = self._workspace(T)
-        r = self.route(x, want_logits)
+        stage = timer if timer is not None else _no_timer
+        with stage("route"):
+            r = self.route(x, want_logits)
         k1 = self.top_k == 1
-        kernels.permute(x, r.gate, r.scan, r.capacity, r.rows, y_zero=out if k1 else None,
-                        out=r.perm)
+        with stage("permute"):
+            kernels.permute(x, r.gate, r.scan, r.capacity, r.rows, y_zero=out if k1 else None,
+                            out=r.perm)
         dst = out if k1 else ws["y_perm"]
-        kernels.grouped_ffn(r.perm.x_perm, self.pool.data, self.d_ff, ACTS[self.act],
-                            r.scan.group_kept, r.scan.group_base, self.group_slot, ws["h"], dst,
-                            row_token=r.perm.row_token if k1 else None,
-                            row_prob=r.perm.row_prob if k1 else None)
+        n1 = 2 * self.d_ff if self.act == "swiglu" else self.d_ff
+        with stage("ffn1"):
+            kernels.grouped_gemm(r.perm.x_perm, self.pool.data, 0, n1, r.scan.group_kept,
+                                 r.scan.group_base, self.group_slot,
+                                 kernels.EPI_SWIGLU if self.act == "swiglu" else kernels.EPI_RELU,
+                                 ws["h"])
+        with stage("ffn2"):
+            kernels.grouped_gemm(ws["h"], self.pool.data, n1 * self.d, self.d, r.scan.group_kept,
+                                 r.scan.group_base, self.group_slot,
+                                 kernels.EPI_SCALE_SCATTER if k1 else kernels.EPI_STORE, dst,
+                                 row_token=r.perm.row_token if k1 else None,
+                                 row_prob=r.perm.row_prob if k1 else None)
         if not k1:
-            kernels.combine(ws["y_perm"], r.perm.token_pos, r.gate.gate_prob, out=out)
+            with stage("combine"):
+                kernels.combine(ws["y_perm"], r.perm.token_pos, r.gate.gate_prob, out=out)
         self.last = r
         return out
 

@@ -47,8 +47,9 @@ def test_merge_f64_bit_exact_vs_reference_checksums():
         f = np.asarray(case["counts"])
         Vd = torch.as_tensor(V, device="cuda")
         out = torch.empty(case["D"], dtype=torch.float64, device="cuda")
-        if f.sum() > 0:
-            w, div = list(f), float(f.sum())
+        freqs = f / max(int(f.sum()), 1)   # stats.freqs: counts / totals
+        if freqs.sum() > 1e-12:
+            w, div = list(freqs), float(freqs.sum())
         else:
             w, div = [1.0] * case["n"], float(case["n"])
         kernels.merge_groups([[Vd[i] for i in range(case["n"])]], [w], [div], [out], torch.float64)
