@@ -165,8 +165,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * EP;
 
-      // online softmax + running top-2 over the logits of this token
-      float m = -INFINITY, s = 0.f;
+      // pass 1: running top-2 over this token's logits (branch-free selects;
+      // strict '>' while scanning ascending expert ids keeps the lowest id on ties)
       float v1 = -INFINITY, v2 = -INFINITY;
       int i1 = -1, i2 = -1;
       float* lrow = (p.logits && valid) ? p.logits + static_cast<long>(t) * p.E : nullptr;
@@ -178,72 +178,100 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const int e = c + j;
-          if (e < p.E) {
+          const float v = e < p.E ? __uint_as_float(r[j]) : -INFINITY;
+          const bool g1 = v > v1, g2 = v > v2;
+          v2 = g1 ? v1 : (g2 ? v : v2);
+          i2 = g1 ? i1 : (g2 ? e : i2);
+          v1 = g1 ? v : v1;
+          i1 = g1 ? e : i1;
+        }
+        if (lrow) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (c + j < p.E) lrow[c + j] = __uint_as_float(r[j]);
+        }
+      }
+      // pass 2 (only when a probability needs the full softmax denominator):
+      // s = sum_e exp(v_e - max), four independent partial sums for ILP
+      float s = 1.f;
+      const bool need_sum = !p.norm_topk;
+      if (need_sum) {
+        constexpr float kLog2e = 1.4426950408889634f;
+        const float mb = v1 * kLog2e;
+        float s4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 1
+        for (int c = 0; c < EP; c += 16) {
+          uint32_t r[16];
+          tmem_ld16(t_row + c, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
             const float v = __uint_as_float(r[j]);
-            if (lrow) lrow[e] = v;
-            if (v > m) {
-              s = s * expf(m - v) + 1.f;
-              m = v;
-            } else {
-              s += expf(v - m);
-            }
-            if (v > v1) {
-              v2 = v1; i2 = i1; v1 = v; i1 = e;
-            } else if (v > v2) {
-              v2 = v; i2 = e;
-            }
+            s4[j & 3] += (c + j < p.E) ? exp2f(fmaf(v, kLog2e, -mb)) : 0.f;
           }
         }
+        s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty_bar[acc]);
 
-      float pr[kGateMaxK];
-      int ex[kGateMaxK], gr[kGateMaxK];
-      ex[0] = i1; ex[1] = i2;
+      // probabilities, slot remap, top-2 fold (all in registers)
+      float pr0, pr1 = 0.f;
       if (p.top_k == 1) {
-        pr[0] = p.norm_topk ? 1.f : 1.f / s;
-        pr[1] = 0.f;
+        pr0 = p.norm_topk ? 1.f : 1.f / s;
       } else if (p.norm_topk) {
         const float z = expf(v2 - v1);
-        pr[0] = 1.f / (1.f + z);
-        pr[1] = z / (1.f + z);
+        pr0 = 1.f / (1.f + z);
+        pr1 = z / (1.f + z);
       } else {
-        pr[0] = expf(v1 - m) / s;
-        pr[1] = expf(v2 - m) / s;
+        pr0 = 1.f / s;
+        pr1 = expf(v2 - v1) / s;
       }
-      for (int j = 0; j < kGateMaxK; ++j)
-        gr[j] = (valid && j < p.top_k && ex[j] >= 0) ? smap[ex[j]] : -1;
-      if (p.top_k == 2 && gr[1] >= 0 && gr[1] == gr[0]) {  // both picks merged into one expert
-        pr[0] += pr[1];
-        pr[1] = 0.f;
-        gr[1] = -1;
+      int gr0 = (valid && i1 >= 0) ? smap[i1] : -1;
+      int gr1 = (valid && p.top_k == 2 && i2 >= 0) ? smap[i2] : -1;
+      if (gr1 >= 0 && gr1 == gr0) {  // both picks merged into one expert
+        pr0 += pr1;
+        pr1 = 0.f;
+        gr1 = -1;
       }
 
       // token-order ranks inside the tile: warp match + per-warp counts
       named_bar_sync(1, 128);
       for (int i = threadIdx.x - 128; i < p.top_k * 4 * kGateMaxE; i += 128) cnt[i] = 0;
       named_bar_sync(1, 128);
-      int wrank[kGateMaxK];
-      for (int j = 0; j < p.top_k; ++j) {
-        const unsigned mask = __match_any_sync(0xffffffffu, gr[j]);
-        wrank[j] = __popc(mask & lt_mask);
-        if (gr[j] >= 0 && wrank[j] == 0) cnt[(j * 4 + q) * kGateMaxE + gr[j]] = __popc(mask);
+      int wr0, wr1 = 0;
+      {
+        const unsigned m0 = __match_any_sync(0xffffffffu, gr0);
+        wr0 = __popc(m0 & lt_mask);
+        if (gr0 >= 0 && wr0 == 0) cnt[q * kGateMaxE + gr0] = __popc(m0);
+        if (p.top_k == 2) {
+          const unsigned m1 = __match_any_sync(0xffffffffu, gr1);
+          wr1 = __popc(m1 & lt_mask);
+          if (gr1 >= 0 && wr1 == 0) cnt[(4 + q) * kGateMaxE + gr1] = __popc(m1);
+        }
       }
       named_bar_sync(1, 128);
       if (valid) {
-        for (int j = 0; j < p.top_k; ++j) {
-          int rank = -1;
-          if (gr[j] >= 0) {
-            rank = wrank[j];
-            for (int qq = 0; qq < q; ++qq) rank += cnt[(j * 4 + qq) * kGateMaxE + gr[j]];
-          }
-          const long o = static_cast<long>(t) * p.top_k + j;
-          p.expert_idx[o] = ex[j];
-          p.group_idx[o] = gr[j];
-          p.gate_prob[o] = gr[j] >= 0 ? pr[j] : 0.f;
-          p.local_rank[o] = rank;
+        int rank0 = -1, rank1 = -1;
+        if (gr0 >= 0) {
+          rank0 = wr0;
+          for (int qq = 0; qq < q; ++qq) rank0 += cnt[qq * kGateMaxE + gr0];
+        }
+        if (gr1 >= 0) {
+          rank1 = wr1;
+          for (int qq = 0; qq < q; ++qq) rank1 += cnt[(4 + qq) * kGateMaxE + gr1];
+        }
+        const long o = static_cast<long>(t) * p.top_k;
+        p.expert_idx[o] = i1;
+        p.group_idx[o] = gr0;
+        p.gate_prob[o] = gr0 >= 0 ? pr0 : 0.f;
+        p.local_rank[o] = rank0;
+        if (p.top_k == 2) {
+          p.expert_idx[o + 1] = i2;
+          p.group_idx[o + 1] = gr1;
+          p.gate_prob[o + 1] = gr1 >= 0 ? pr1 : 0.f;
+          p.local_rank[o + 1] = rank1;
         }
       }
       for (int j = 0; j < p.top_k; ++j)

@@ -49,9 +49,11 @@ struct GemmSmem {
   static constexpr int kBBytes = BN * kGemmBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTileBytes = kStages * kStageBytes;
+  // epilogue staging: 4 warps x (32 rows x 128 B), 128B-swizzled chunks
+  static constexpr int kStageOutBytes = 4 * 32 * 128;
   // barriers + tmem slot + tile prefix table
   static constexpr int kCtrlBytes = (2 * kStages + 4) * 8 + 16 + (kMaxGroups + 1) * 4;
-  static constexpr int kTotal = 1024 /*align slack*/ + kTileBytes + kCtrlBytes;
+  static constexpr int kTotal = 1024 /*align slack*/ + kTileBytes + kStageOutBytes + kCtrlBytes;
 };
 
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
@@ -117,7 +119,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + kStages * S::kABytes;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S::kTileBytes);
+  uint8_t* smem_out = smem + S::kTileBytes;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S::kTileBytes + S::kStageOutBytes);
   uint64_t* empty_bar = full_bar + kStages;
   uint64_t* tfull_bar = empty_bar + kStages;   // [2]
   uint64_t* tempty_bar = tfull_bar + 2;        // [2]
@@ -202,7 +205,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else if (warp >= 4) {
     // ------------------------------------------------ epilogue
+    // TMEM -> registers (thread = row) -> bf16 -> swizzled smem staging ->
+    // warp-cooperative stores of whole 128-byte row segments (8 lanes/row),
+    // so every store instruction touches 4 full lines instead of 32 partial ones.
     const int q = warp & 3;  // TMEM lane quarter this warp may access
+    uint8_t* stg = smem_out + q * (32 * 128);
+    const int sub_row = lane >> 3, sub_chunk = lane & 7;
     int it = 0;
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
       const int acc = it & 1;
@@ -211,58 +219,48 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int local = tile - prefix[g];
       const int mt = local / n_tiles, nt = local % n_tiles;
       const int rows = __ldg(p.group_rows + g);
-      const int r = mt * kGemmBM + q * 32 + lane;
-      const bool valid = r < rows;
-      const long arow = static_cast<long>(__ldg(p.group_row_base + g)) + r;
-
-      __nv_bfloat16* dst = nullptr;
+      const int r0 = mt * kGemmBM + q * 32;  // first row (within the group) of this warp
+      const long arow0 = static_cast<long>(__ldg(p.group_row_base + g)) + r0;
+      const bool valid = r0 + lane < rows;
+      long my_row = -1;  // destination row of this thread's accumulator row
       float scale = 1.f;
       if (valid) {
         if constexpr (kMode == kEpiScaleScatter) {
-          const int tok = __ldg(p.row_token + arow);
-          scale = __ldg(p.row_prob + arow);
-          dst = p.out + static_cast<long>(tok) * p.ldo + nt * BN;
-        } else if constexpr (kMode == kEpiSwiGLU) {
-          dst = p.out + arow * p.ldo + nt * (BN / 2);
+          my_row = __ldg(p.row_token + arow0 + lane);
+          scale = __ldg(p.row_prob + arow0 + lane);
         } else {
-          dst = p.out + arow * p.ldo + nt * BN;
+          my_row = arow0 + lane;
         }
       }
+      constexpr int kOutCols = kMode == kEpiSwiGLU ? BN / 2 : BN;
+      const long col0 = static_cast<long>(nt) * kOutCols;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
-
-      if constexpr (kMode == kEpiSwiGLU) {
 #pragma unroll 1
-        for (int c = 0; c < BN / 2; c += 32) {
-          uint32_t gv[32], uv[32];
-          tmem_ld32(t_row + c, gv);
-          tmem_ld32(t_row + BN / 2 + c, uv);
-          tmem_ld_wait();
-          if (valid) {
-            uint32_t packed[16];
+      for (int c = 0; c < kOutCols; c += 64) {
+        uint32_t packed[32];
+        if constexpr (kMode == kEpiSwiGLU) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            uint32_t gv[32], uv[32];
+            tmem_ld32(t_row + c + 32 * h, gv);
+            tmem_ld32(t_row + BN / 2 + c + 32 * h, uv);
+            tmem_ld_wait();
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-              float g0 = __uint_as_float(gv[2 * j]), g1 = __uint_as_float(gv[2 * j + 1]);
-              float u0 = __uint_as_float(uv[2 * j]), u1 = __uint_as_float(uv[2 * j + 1]);
-              float h0 = g0 / (1.f + __expf(-g0)) * u0;
-              float h1 = g1 / (1.f + __expf(-g1)) * u1;
-              packed[j] = pack_bf16x2(h0, h1);
+              const float g0 = __uint_as_float(gv[2 * j]), g1 = __uint_as_float(gv[2 * j + 1]);
+              const float u0 = __uint_as_float(uv[2 * j]), u1 = __uint_as_float(uv[2 * j + 1]);
+              packed[16 * h + j] = pack_bf16x2(g0 / (1.f + __expf(-g0)) * u0,
+                                               g1 / (1.f + __expf(-g1)) * u1);
             }
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              st_global_v4(dst + c + 8 * j, packed[4 * j], packed[4 * j + 1], packed[4 * j + 2],
-                           packed[4 * j + 3]);
           }
-        }
-      } else {
-#pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
-          uint32_t v[32];
-          tmem_ld32(t_row + c, v);
-          tmem_ld_wait();
-          if (valid) {
-            uint32_t packed[16];
+        } else {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            uint32_t v[32];
+            tmem_ld32(t_row + c + 32 * h, v);
+            tmem_ld_wait();
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
               float a0 = __uint_as_float(v[2 * j]), a1 = __uint_as_float(v[2 * j + 1]);
@@ -273,14 +271,32 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 a0 *= scale;
                 a1 *= scale;
               }
-              packed[j] = pack_bf16x2(a0, a1);
+              packed[16 * h + j] = pack_bf16x2(a0, a1);
             }
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              st_global_v4(dst + c + 8 * j, packed[4 * j], packed[4 * j + 1], packed[4 * j + 2],
-                           packed[4 * j + 3]);
           }
         }
+        // stage my row: 8 chunks of 16 B, chunk j at (j ^ row%8) — conflict-free both ways
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t a = smem_u32(stg + lane * 128 + ((j ^ (lane & 7)) << 4));
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(packed[4 * j]),
+                       "r"(packed[4 * j + 1]), "r"(packed[4 * j + 2]), "r"(packed[4 * j + 3])
+                       : "memory");
+        }
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int row = 4 * k + sub_row;
+          const long dst_row = __shfl_sync(0xffffffffu, my_row, row);
+          const uint32_t a = smem_u32(stg + row * 128 + ((sub_chunk ^ (row & 7)) << 4));
+          uint32_t x0, x1, x2, x3;
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3)
+                       : "r"(a));
+          if (dst_row >= 0)
+            st_global_v4(p.out + dst_row * p.ldo + col0 + c + sub_chunk * 8, x0, x1, x2, x3);
+        }
+        __syncwarp();
       }
       tc_fence_before();
       __syncwarp();
