@@ -1,0 +1,160 @@
+"""Expert parallelism: experts block-partitioned over ranks, tokens data-
+parallel, one NCCL all-to-all each way.
+
+Per rank (T_g tokens, E experts, E_l = E / world local experts):
+  gate (local, replicated router) -> scan -> permute straight into the send
+  buffer laid out [dst rank][local expert][C_g][d] (fixed per-(source, expert)
+  capacity C_g = ceil(cf*T_g*k/E), so every all-to-all chunk has the same
+  size and no host synchronisation is needed)
+  -> all_to_all(counts), all_to_all(rows)
+  -> grouped FFN over (source rank, local expert) groups of the receive buffer
+  -> all_to_all(rows back) -> combine (token_pos addresses the fixed layout).
+
+The collective schedule lives in `ep_forward`, written once against an `ops`
+object: `DeviceOps` calls the sm_100a kernels; tests pass a CPU double so the
+N>1 data movement is exercised with gloo on a CPU-only box. Capacity is per
+token group (GShard/Switch), so rank r's outputs equal a single-device
+forward over rank r's tokens.
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from . import kernels
+from .pool import ExpertPool
+
+
+def ep_capacity(tokens_per_rank: int, n_experts: int, top_k: int, capacity_factor) -> int:
+    return kernels.capacity_for(tokens_per_rank, n_experts, top_k, capacity_factor)
+
+
+def ep_forward(x, ops, world: int, n_experts: int, capacity: int, group=None):
+    """One EP layer forward of this rank's tokens `x` [T_g, d]."""
+    E, C = n_experts, capacity
+    El = E // world
+    route = ops.route(x)                                # gate + scan (counts per global expert)
+    send_rows, token_pos = ops.dispatch(x, route, C)    # [E*C, d] fixed layout
+    kept = route.kept                                   # [E] int32, rows per expert from me
+    recv_counts = torch.empty_like(kept)
+    dist.all_to_all_single(recv_counts, kept, group=group)
+    recv_rows = torch.empty_like(send_rows)
+    dist.all_to_all_single(recv_rows, send_rows, group=group)
+    # groups on the receiver: (src, local expert) -> rows recv_counts[src*El+le]
+    y_recv = ops.expert_ffn(recv_rows, recv_counts, El, C, world)
+    y_back = torch.empty_like(y_recv)
+    dist.all_to_all_single(y_back, y_recv, group=group)
+    return ops.combine(y_back, token_pos, route)
+
+
+class DeviceOps:
+    """ep_forward ops backed by the CUDA kernels; owns the EP buffers."""
+
+    def __init__(self, layer):
+        self.layer = layer
+        self._bufs = {}
+
+    def _buf(self, key, make):
+        if key not in self._bufs:
+            self._bufs[key] = make()
+        return self._bufs[key]
+
+    def route(self, x):
+        r = self.layer.route(x)
+        r.kept = r.scan.group_kept
+        self.layer.last = r
+        return r
+
+    def dispatch(self, x, route, C):
+        L = self.layer
+        dev, T, E, d = x.device, x.shape[0], L.E, L.d
+        rows = E * C
+        base = self._buf(("base", E, C),
+                         lambda: torch.arange(E, dtype=torch.int32, device=dev) * C)
+        perm = self._buf(("perm", T, rows), lambda: kernels.PermuteOutput(
+            torch.zeros((rows, d), dtype=torch.bfloat16, device=dev),
+            torch.empty(rows, dtype=torch.int32, device=dev),
+            torch.empty(rows, dtype=torch.float32, device=dev),
+            torch.empty((T, L.top_k), dtype=torch.int32, device=dev)))
+        fixed = kernels.ScanOutput(route.scan.tile_offset, route.scan.group_count,
+                                   route.scan.group_kept, base)
+        kernels.permute(x, route.gate, fixed, C, rows, y_zero=None, out=perm)
+        return perm.x_perm, perm.token_pos
+
+    def expert_ffn(self, recv_rows, recv_counts, El, C, world):
+        L = self.layer
+        dev = recv_rows.device
+        G = world * El
+        base = self._buf(("gbase", G, C),
+                         lambda: torch.arange(G, dtype=torch.int32, device=dev) * C)
+        slot = self._buf(("gslot", G, El),
+                         lambda: (torch.arange(G, dtype=torch.int32, device=dev) % El).contiguous())
+        rows = recv_rows.shape[0]
+        h = self._buf(("h", rows), lambda: torch.empty((rows, L.d_ff), dtype=torch.bfloat16,
+                                                       device=dev))
+        y = self._buf(("y", rows), lambda: torch.empty_like(recv_rows))
+        n1 = 2 * L.d_ff if L.act == "swiglu" else L.d_ff
+        kernels.grouped_gemm(recv_rows, L.pool.data, 0, n1, recv_counts, base, slot,
+                             kernels.EPI_SWIGLU if L.act == "swiglu" else kernels.EPI_RELU, h)
+        kernels.grouped_gemm(h, L.pool.data, n1 * L.d, L.d, recv_counts, base, slot,
+                             kernels.EPI_STORE, y)
+        return y
+
+    def combine(self, y_back, token_pos, route):
+        return kernels.combine(y_back, token_pos, route.gate.gate_prob)
+
+
+class EPMoELayer:
+    """MoE layer with experts sharded over the ranks of `group`.
+
+    Holds the full router and this rank's E/world experts in an ExpertPool
+    (local slot le = global expert rank*E_l + le)."""
+
+    def __init__(self, wg, pool: ExpertPool, d_ff: int, world: int, rank: int, act="relu",
+                 top_k=1, norm_topk=None, capacity_factor=1.25, group=None):
+        from .layer import MoELayer
+        d, E = wg.shape
+        if E % world:
+            raise ValueError(f"{E} experts do not split over {world} ranks")
+        if pool.n_slots < E // world:
+            raise ValueError("pool must hold this rank's E/world experts")
+        self.world, self.rank, self.E, self.El = world, rank, E, E // world
+        self.group = group
+        self.capacity_factor = capacity_factor
+        # gate/scan run on all E experts; with G = E groups the per-rank
+        # capacity of MoELayer equals the EP capacity ceil(cf*T_g*k/E)
+        self.local = MoELayer(wg, pool, d_ff, act=act, top_k=top_k, norm_topk=norm_topk,
+                              capacity_factor=capacity_factor, expert_slots=[0] * E)
+        self.ops = DeviceOps(self.local)
+
+    @classmethod
+    def synthetic(cls, wg, d_ff, E, world, rank, capacity_factor=1.25, seed=2, act="relu"):
+        d = wg.shape[0]
+        numel = kernels.expert_numel(d, d_ff, kernels.ACT_SWIGLU if act == "swiglu" else kernels.ACT_RELU)
+        pool = ExpertPool(E // world, numel, device=wg.device)
+        pool.data.normal_(0.0, 0.02,
+                          generator=torch.Generator(device=wg.device).manual_seed(seed + rank))
+        return cls(wg, pool, d_ff, world, rank, act=act, capacity_factor=capacity_factor)
+
+    def capacity(self, T: int) -> int:
+        return ep_capacity(T, self.E, self.local.top_k, self.capacity_factor)
+
+    @property
+    def last(self):
+        return self.local.last
+
+    def forward(self, x, out=None, timer=None):
+        y = ep_forward(x, self.ops, self.world, self.E, self.capacity(x.shape[0]),
+                       group=self.group)
+        if out is not None:
+            out.copy_(y)
+            return out
+        return y
+
+    __call__ = forward
+
+    @property
+    def kernels_per_forward(self) -> int:
+        # gate, 2x scan, permute, 2x GEMM, combine (NCCL's all-to-all kernels not counted)
+        return 7
