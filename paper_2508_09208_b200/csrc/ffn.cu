@@ -3,7 +3,9 @@
 // [W_in (N1 x d) | W_out (d x d_ff)], N1 = d_ff (ReLU) or 2*d_ff (SwiGLU with
 // gate/up interleaved in 128-row blocks) — the device image of the
 // reference's flat `Expert.params` (pkg/src/comoe/moe.py:69-74).
-#include "grouped_gemm.cuh"
+#include <cstdlib>
+
+#include "grouped_gemm_2sm.cuh"
 #include "../../include/comoe_b200.h"
 
 namespace comoe {
@@ -23,6 +25,30 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const Group
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   kern<<<sms, kGemmThreads, S::kTotal, stream>>>(ta, tb, p);
   return check_launch("grouped_gemm_kernel");
+}
+
+template <int kMode>
+static int launch_gemm_2sm(const CUtensorMap& tw, const CUtensorMap& tx,
+                           const GroupedGemmParams& p, cudaStream_t stream) {
+  auto kern = grouped_gemm_2sm_kernel<kMode>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Gemm2Smem::kTotal);
+    attr_set = true;
+  }
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  kern<<<sms & ~1, kGemmThreads, Gemm2Smem::kTotal, stream>>>(tw, tx, p);
+  return check_launch("grouped_gemm_2sm_kernel");
+}
+
+static bool force_1sm() {
+  static const bool f = [] {
+    const char* e = std::getenv("COMOE_GEMM_1SM");
+    return e && e[0] == '1';
+  }();
+  return f;
 }
 
 // B operand: `N x K` matrix at element offset `b_offset` inside every slot.
@@ -46,13 +72,29 @@ static int grouped_gemm_impl(const void* a, long a_rows, const void* pool, int n
   if (epi_mode == kEpiScaleScatter)
     COMOE_REQUIRE(row_token && row_prob, kBadArg, "scatter epilogue needs row_token/row_prob");
   CUtensorMap ta, tb;
-  int rc = make_tmap_bf16_2d(&ta, a, static_cast<uint64_t>(a_rows), K, kGemmBM);
-  if (rc) return rc;
   const void* b = static_cast<const __nv_bfloat16*>(pool) + b_offset;
-  rc = make_tmap_bf16_3d(&tb, b, n_slots, N, K, slot_stride, 256);
-  if (rc) return rc;
   GroupedGemmParams p{group_rows, group_row_base, group_slot, G, N, K,
                       reinterpret_cast<__nv_bfloat16*>(out), ldo, row_token, row_prob};
+  int rc;
+  if (epi_mode != kEpiSwiGLU && !force_1sm()) {
+    // 2-SM swap-AB kernel: weights = A (128-feature boxes), tokens = B (128-row boxes)
+    rc = make_tmap_bf16_3d(&tb, b, n_slots, N, K, slot_stride, 128);
+    if (rc) return rc;
+    rc = make_tmap_bf16_2d(&ta, a, static_cast<uint64_t>(a_rows), K, 128);
+    if (rc) return rc;
+    switch (epi_mode) {
+      case kEpiRelu: return launch_gemm_2sm<kEpiRelu>(tb, ta, p, stream);
+      case kEpiScaleScatter: return launch_gemm_2sm<kEpiScaleScatter>(tb, ta, p, stream);
+      case kEpiStore: return launch_gemm_2sm<kEpiStore>(tb, ta, p, stream);
+      default: break;
+    }
+    set_error("grouped_gemm: unknown epilogue mode %d", epi_mode);
+    return kBadArg;
+  }
+  rc = make_tmap_bf16_2d(&ta, a, static_cast<uint64_t>(a_rows), K, kGemmBM);
+  if (rc) return rc;
+  rc = make_tmap_bf16_3d(&tb, b, n_slots, N, K, slot_stride, 256);
+  if (rc) return rc;
   switch (epi_mode) {
     case kEpiRelu: return launch_gemm<256, 4, kEpiRelu>(ta, tb, p, stream);
     case kEpiSwiGLU: return launch_gemm<256, 4, kEpiSwiGLU>(ta, tb, p, stream);

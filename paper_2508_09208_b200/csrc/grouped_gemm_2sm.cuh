@@ -1,0 +1,320 @@
+// K3 (2-SM variant): grouped expert GEMM on CTA pairs (tcgen05 cta_group::2).
+//
+// Swap-AB formulation: the expert weights are the MMA "A" operand (M = 256
+// output features per CTA pair, 128 per SM) and the routed token rows are
+// the "B" operand (N = up to 256 tokens, any multiple of 16, chosen per
+// tile at run time). Consequences:
+//   * ragged expert groups waste < 16 token columns per group instead of up
+//     to 127 rows of a 128-row M tile;
+//   * each SM stages only half of each operand (A: its 128 features, B: its
+//     N/2 tokens) — half the shared-memory operand traffic of the 1-SM
+//     128x256 tile, the limiter measured in profiles/r1 (tensor pipe ~66%).
+// D[feature, token] lands in TMEM (lanes = features, columns = tokens);
+// the epilogue transposes 32x32 blocks through shared memory so every
+// global store writes whole 256-byte token-row segments.
+#pragma once
+
+#include "grouped_gemm.cuh"
+
+namespace comoe {
+
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // clear the peer-CTA bit -> leader's smem
+constexpr int k2BM = 256;                    // features per CTA pair
+constexpr int k2BN = 256;                    // max tokens per tile
+constexpr int k2Stages = 5;
+
+struct Gemm2Smem {
+  static constexpr int kABytes = 128 * kGemmBK * 2;  // 128 feature rows x 64 K
+  static constexpr int kBBytes = 128 * kGemmBK * 2;  // up to 128 token rows x 64 K
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kTileBytes = k2Stages * kStageBytes;
+  static constexpr int kXposeBytes = 4 * 32 * 33 * 4;   // per-warp fp32 32x33 transpose
+  static constexpr int kStgBytes = 32 * 256;             // 32 tokens x 128 features bf16
+  static constexpr int kCtrlBytes = (2 * k2Stages + 4) * 8 + 16 + (kMaxGroups + 1) * 4;
+  static constexpr int kTotal = 1024 + kTileBytes + kXposeBytes + kStgBytes + kCtrlBytes;
+};
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, uint32_t bar,
+                                                int32_t x, int32_t y, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_2sm(void* dst, const CUtensorMap* map, uint32_t bar,
+                                                int32_t x, int32_t y, int32_t z, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y), "r"(z), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void umma_bf16_2sm(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit_2sm_mc(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], m;\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
+// tiles of a group: ceil(rows/256) token tiles x (N/256) feature tiles
+__device__ __forceinline__ void build_tile_prefix_2sm(const int* __restrict__ rows, int G,
+                                                      int f_tiles, int* prefix) {
+  __shared__ int warp_tot2[kGemmThreads / 32];
+  const int tid = threadIdx.x;
+  const int per = (G + kGemmThreads - 1) / kGemmThreads;
+  const int g0 = tid * per;
+  int local = 0;
+  for (int i = 0; i < per; ++i)
+    if (g0 + i < G) local += ((__ldg(rows + g0 + i) + k2BN - 1) / k2BN) * f_tiles;
+  int v = local;
+  const int lane = tid & 31, w = tid >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int n = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += n;
+  }
+  if (lane == 31) warp_tot2[w] = v;
+  __syncthreads();
+  int run = v - local;
+  for (int i = 0; i < w; ++i) run += warp_tot2[i];
+  for (int i = 0; i < per; ++i) {
+    const int g = g0 + i;
+    if (g < G) {
+      prefix[g] = run;
+      run += ((__ldg(rows + g) + k2BN - 1) / k2BN) * f_tiles;
+    }
+  }
+  if (tid == kGemmThreads - 1) prefix[G] = run;
+  __syncthreads();
+}
+
+struct Tile2 {
+  int g, ft, tok0, ntok, nmma;
+};
+
+__device__ __forceinline__ Tile2 decode_tile2(const int* prefix, const GroupedGemmParams& p,
+                                              int f_tiles, int tile) {
+  Tile2 t;
+  t.g = find_group(prefix, p.G, tile);
+  const int local = tile - prefix[t.g];
+  const int tt = local / f_tiles;
+  t.ft = local % f_tiles;
+  t.tok0 = tt * k2BN;
+  const int rows = __ldg(p.group_rows + t.g);
+  t.ntok = min(k2BN, rows - t.tok0);
+  t.nmma = (t.ntok + 15) & ~15;
+  return t;
+}
+
+template <int kMode>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
+    grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmap_w,
+                            const __grid_constant__ CUtensorMap tmap_x, GroupedGemmParams p) {
+  static_assert(kMode != kEpiSwiGLU, "SwiGLU uses the 1-SM kernel");
+  using S = Gemm2Smem;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* smem_a = smem;                                   // weights
+  uint8_t* smem_b = smem + k2Stages * S::kABytes;           // tokens
+  float* xpose = reinterpret_cast<float*>(smem + S::kTileBytes);
+  uint8_t* stg = smem + S::kTileBytes + S::kXposeBytes;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(stg + S::kStgBytes);
+  uint64_t* empty_bar = full_bar + k2Stages;
+  uint64_t* tfull_bar = empty_bar + k2Stages;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  int* prefix = reinterpret_cast<int*>(tmem_slot + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int f_tiles = p.N / k2BM;
+  const int k_blocks = p.K / kGemmBK;
+  const int n_clusters = gridDim.x >> 1;
+  const int cluster = blockIdx.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_w);
+    tma_prefetch_desc(&tmap_x);
+    for (int s = 0; s < k2Stages; ++s) {
+      mbar_init(&full_bar[s], 2);   // one arrive per CTA of the pair (leader's copy is used)
+      mbar_init(&empty_bar[s], 1);  // MMA commit multicast
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  build_tile_prefix_2sm(p.group_rows, p.G, f_tiles, prefix);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int total_tiles = prefix[p.G];
+
+  if (warp == 0) {
+    // ---------------------------------------------- TMA producer (both CTAs)
+    if (elect_one()) {
+      const uint64_t pol_w = l2_policy_evict_last();
+      const uint64_t pol_x = l2_policy_evict_first();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cluster; tile < total_tiles; tile += n_clusters) {
+        const Tile2 t = decode_tile2(prefix, p, f_tiles, tile);
+        const int slot = __ldg(p.group_slot + t.g);
+        const int feat = t.ft * k2BM + static_cast<int>(rank) * 128;
+        const int tok = __ldg(p.group_row_base + t.g) + t.tok0 + static_cast<int>(rank) * (t.nmma >> 1);
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          const uint32_t fb = smem_u32(&full_bar[stage]) & kPeerMask;
+          if (leader) mbar_expect_tx(&full_bar[stage], 2 * S::kStageBytes);
+          else mbar_arrive_cluster(fb);
+          tma_load_3d_2sm(smem_a + stage * S::kABytes, &tmap_w, fb, kb * kGemmBK, feat, slot, pol_w);
+          tma_load_2d_2sm(smem_b + stage * S::kBBytes, &tmap_x, fb, kb * kGemmBK, tok, pol_x);
+          if (++stage == k2Stages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------- MMA issuer (leader CTA only)
+    if (leader && elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = cluster; tile < total_tiles; tile += n_clusters, ++it) {
+        const Tile2 t = decode_tile2(prefix, p, f_tiles, tile);
+        const uint32_t idesc = umma_idesc_bf16_f32(k2BM, t.nmma);
+        const int acc = it & 1;
+        mbar_wait(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * k2BN;
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint64_t adesc = umma_desc_k_sw128(smem_u32(smem_a + stage * S::kABytes));
+          const uint64_t bdesc = umma_desc_k_sw128(smem_u32(smem_b + stage * S::kBBytes));
+#pragma unroll
+          for (int k = 0; k < kGemmBK / 16; ++k)
+            umma_bf16_2sm(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+          umma_commit_2sm_mc(&empty_bar[stage]);
+          if (++stage == k2Stages) { stage = 0; phase ^= 1; }
+        }
+        umma_commit_2sm_mc(&tfull_bar[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------------------------------------- epilogue (both CTAs)
+    const int q = warp & 3;                       // features 32q..32q+31 of this SM's 128
+    float* xp = xpose + q * (32 * 33);
+    int it = 0;
+    for (int tile = cluster; tile < total_tiles; tile += n_clusters, ++it) {
+      const Tile2 t = decode_tile2(prefix, p, f_tiles, tile);
+      const int acc = it & 1;
+      const long row_base = static_cast<long>(__ldg(p.group_row_base + t.g)) + t.tok0;
+      const long col0 = static_cast<long>(t.ft) * k2BM + rank * 128;  // first output feature
+      mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * k2BN;
+      for (int c = 0; c < t.nmma; c += 32) {
+        uint32_t v[32];
+        tmem_ld32(t_row + c, v);
+        tmem_ld_wait();
+        if (c + 32 >= t.nmma) {  // accumulator fully read: release it to the MMA
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(smem_u32(&tempty_bar[acc]) & kPeerMask);
+        }
+        // transpose 32 features x 32 tokens through padded smem (conflict-free)
+#pragma unroll
+        for (int j = 0; j < 32; ++j) xp[lane * 33 + j] = __uint_as_float(v[j]);
+        __syncwarp();
+        const int tok = c + lane;  // token (column) this thread now owns
+        const bool tvalid = tok < t.ntok;
+        float scale = 1.f;
+        if constexpr (kMode == kEpiScaleScatter) scale = tvalid ? __ldg(p.row_prob + row_base + tok) : 0.f;
+        uint32_t packed[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          float a0 = xp[(2 * j) * 33 + lane], a1 = xp[(2 * j + 1) * 33 + lane];
+          if constexpr (kMode == kEpiRelu) {
+            a0 = fmaxf(a0, 0.f);
+            a1 = fmaxf(a1, 0.f);
+          } else if constexpr (kMode == kEpiScaleScatter) {
+            a0 *= scale;
+            a1 *= scale;
+          }
+          packed[j] = pack_bf16x2(a0, a1);
+        }
+        // stage [32 tokens][128 features] bf16, 16B chunks XOR-swizzled by token
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int chunk = (4 * q + j) ^ (lane & 15);
+          const uint32_t a = smem_u32(stg + lane * 256 + chunk * 16);
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(packed[4 * j]),
+                       "r"(packed[4 * j + 1]), "r"(packed[4 * j + 2]), "r"(packed[4 * j + 3])
+                       : "memory");
+        }
+        named_bar_sync(1, 128);
+        // cooperative stores: warp q writes token rows 8q..8q+7, 16 lanes x 16 B per row
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r = 8 * q + 2 * i + (lane >> 4);
+          const int chunk = lane & 15;
+          const int tk = c + r;
+          const uint32_t a = smem_u32(stg + r * 256 + ((chunk ^ (r & 15)) << 4));
+          uint32_t x0, x1, x2, x3;
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3)
+                       : "r"(a));
+          if (tk < t.ntok) {
+            long dst;
+            if constexpr (kMode == kEpiScaleScatter) dst = __ldg(p.row_token + row_base + tk);
+            else dst = row_base + tk;
+            st_global_v4(p.out + dst * p.ldo + col0 + chunk * 8, x0, x1, x2, x3);
+          }
+        }
+        named_bar_sync(1, 128);
+      }
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base)
+                 : "memory");
+  }
+}
+
+}  // namespace comoe
