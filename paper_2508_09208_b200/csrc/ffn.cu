@@ -39,7 +39,7 @@ static int launch_gemm_2sm(const CUtensorMap& tw, const CUtensorMap& tx,
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  kern<<<sms & ~1, kGemmThreads, Gemm2Smem::kTotal, stream>>>(tw, tx, p);
+  kern<<<sms & ~1, k2Threads, Gemm2Smem::kTotal, stream>>>(tw, tx, p);
   return check_launch("grouped_gemm_2sm_kernel");
 }
 

@@ -21,18 +21,37 @@ namespace comoe {
 constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // clear the peer-CTA bit -> leader's smem
 constexpr int k2BM = 256;                    // features per CTA pair
 constexpr int k2BN = 256;                    // max tokens per tile
-constexpr int k2Stages = 5;
+constexpr int k2Stages = 4;
+constexpr int k2EpiWarps = 8;                     // 2 per TMEM lane quarter
+constexpr int k2Threads = 128 + 32 * k2EpiWarps;  // w0 TMA, w1 MMA, w2 TMEM, w3 idle, w4.. epilogue
 
 struct Gemm2Smem {
   static constexpr int kABytes = 128 * kGemmBK * 2;  // 128 feature rows x 64 K
   static constexpr int kBBytes = 128 * kGemmBK * 2;  // up to 128 token rows x 64 K
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTileBytes = k2Stages * kStageBytes;
-  static constexpr int kXposeBytes = 4 * 32 * 33 * 4;   // per-warp fp32 32x33 transpose
-  static constexpr int kStgBytes = 32 * 256;             // 32 tokens x 128 features bf16
+  static constexpr int kXposeBytes = k2EpiWarps * 32 * 32 * 4;  // per-warp fp32 32x32 transpose
+  static constexpr int kStgBytes = k2EpiWarps * 32 * 64;        // per-warp 32 tokens x 32 features bf16
   static constexpr int kCtrlBytes = (2 * k2Stages + 4) * 8 + 16 + (kMaxGroups + 1) * 4;
   static constexpr int kTotal = 1024 + kTileBytes + kXposeBytes + kStgBytes + kCtrlBytes;
 };
+
+__device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w)
+               : "memory");
+}
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(a));
+  return v;
+}
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
@@ -81,9 +100,9 @@ __device__ __forceinline__ void umma_commit_2sm_mc(uint64_t* bar) {
 // tiles of a group: ceil(rows/256) token tiles x (N/256) feature tiles
 __device__ __forceinline__ void build_tile_prefix_2sm(const int* __restrict__ rows, int G,
                                                       int f_tiles, int* prefix) {
-  __shared__ int warp_tot2[kGemmThreads / 32];
+  __shared__ int warp_tot2[k2Threads / 32];
   const int tid = threadIdx.x;
-  const int per = (G + kGemmThreads - 1) / kGemmThreads;
+  const int per = (G + k2Threads - 1) / k2Threads;
   const int g0 = tid * per;
   int local = 0;
   for (int i = 0; i < per; ++i)
@@ -106,7 +125,7 @@ __device__ __forceinline__ void build_tile_prefix_2sm(const int* __restrict__ ro
       run += ((__ldg(rows + g) + k2BN - 1) / k2BN) * f_tiles;
     }
   }
-  if (tid == kGemmThreads - 1) prefix[G] = run;
+  if (tid == k2Threads - 1) prefix[G] = run;
   __syncthreads();
 }
 
@@ -129,7 +148,7 @@ __device__ __forceinline__ Tile2 decode_tile2(const int* prefix, const GroupedGe
 }
 
 template <int kMode>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k2Threads, 1)
     grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmap_w,
                             const __grid_constant__ CUtensorMap tmap_x, GroupedGemmParams p) {
   static_assert(kMode != kEpiSwiGLU, "SwiGLU uses the 1-SM kernel");
@@ -139,7 +158,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* smem_a = smem;                                   // weights
   uint8_t* smem_b = smem + k2Stages * S::kABytes;           // tokens
-  float* xpose = reinterpret_cast<float*>(smem + S::kTileBytes);
+  uint8_t* xpose = smem + S::kTileBytes;
   uint8_t* stg = smem + S::kTileBytes + S::kXposeBytes;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(stg + S::kStgBytes);
   uint64_t* empty_bar = full_bar + k2Stages;
@@ -165,7 +184,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
+      mbar_init(&tempty_bar[a], 2 * k2EpiWarps);  // epilogue warps of both CTAs (leader's copy)
     }
     fence_barrier_init();
   }
@@ -186,7 +205,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     // ---------------------------------------------- TMA producer (both CTAs)
     if (elect_one()) {
       const uint64_t pol_w = l2_policy_evict_last();
-      const uint64_t pol_x = l2_policy_evict_first();
+      // token rows are re-read by every feature tile of the group: keep them
+      // (evict_first here doubled DRAM reads of H, profiles/r1_2sm_evict_first)
+      const uint64_t pol_x = l2_policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = cluster; tile < total_tiles; tile += n_clusters) {
@@ -234,38 +255,53 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     }
   } else if (warp >= 4) {
     // ---------------------------------------------- epilogue (both CTAs)
-    const int q = warp & 3;                       // features 32q..32q+31 of this SM's 128
-    float* xp = xpose + q * (32 * 33);
+    // Warp w: TMEM lane quarter q = w%4 (features 32q..32q+31 of this SM's
+    // 128), token chunks c = 32*(2j + sub). Per chunk: TMEM -> regs (thread =
+    // feature) -> fp32 transpose in smem (thread = token) -> bf16 row staging
+    // -> 16-byte stores, 4 lanes per 64-byte token-row segment. All smem
+    // layouts are XOR-swizzled on 16-byte chunks: conflict-free both ways.
+    const int ew = warp - 4;
+    const int q = warp & 3, sub = ew >> 2;
+    const uint32_t xp = smem_u32(xpose) + ew * (32 * 32 * 4);
+    const uint32_t sg = smem_u32(stg) + ew * (32 * 64);
     int it = 0;
     for (int tile = cluster; tile < total_tiles; tile += n_clusters, ++it) {
       const Tile2 t = decode_tile2(prefix, p, f_tiles, tile);
       const int acc = it & 1;
       const long row_base = static_cast<long>(__ldg(p.group_row_base + t.g)) + t.tok0;
-      const long col0 = static_cast<long>(t.ft) * k2BM + rank * 128;  // first output feature
+      const long col0 = static_cast<long>(t.ft) * k2BM + rank * 128 + q * 32;
       mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
       tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * k2BN;
-      for (int c = 0; c < t.nmma; c += 32) {
+      const int chunks = (t.nmma + 31) >> 5;
+      bool released = false;
+      for (int ci = sub; ci < chunks; ci += 2) {
+        const int c = ci * 32;
         uint32_t v[32];
         tmem_ld32(t_row + c, v);
         tmem_ld_wait();
-        if (c + 32 >= t.nmma) {  // accumulator fully read: release it to the MMA
+        if (ci + 2 >= chunks) {  // this warp's last TMEM read of the tile
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(smem_u32(&tempty_bar[acc]) & kPeerMask);
+          released = true;
         }
-        // transpose 32 features x 32 tokens through padded smem (conflict-free)
+        // fp32 [feature][token] with chunk' = (token/4) ^ (feature%8)
 #pragma unroll
-        for (int j = 0; j < 32; ++j) xp[lane * 33 + j] = __uint_as_float(v[j]);
+        for (int j = 0; j < 8; ++j)
+          sts128(xp + lane * 128 + ((j ^ (lane & 7)) << 4), v[4 * j], v[4 * j + 1], v[4 * j + 2],
+                 v[4 * j + 3]);
         __syncwarp();
-        const int tok = c + lane;  // token (column) this thread now owns
-        const bool tvalid = tok < t.ntok;
+        const int tok = c + lane;  // this thread now owns token `tok`
         float scale = 1.f;
-        if constexpr (kMode == kEpiScaleScatter) scale = tvalid ? __ldg(p.row_prob + row_base + tok) : 0.f;
+        if constexpr (kMode == kEpiScaleScatter)
+          scale = tok < t.ntok ? __ldg(p.row_prob + row_base + tok) : 0.f;
         uint32_t packed[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          float a0 = xp[(2 * j) * 33 + lane], a1 = xp[(2 * j + 1) * 33 + lane];
+          const int f0 = 2 * j, f1 = 2 * j + 1;
+          float a0 = lds_f32(xp + f0 * 128 + ((((lane >> 2) ^ (f0 & 7))) << 4) + ((lane & 3) << 2));
+          float a1 = lds_f32(xp + f1 * 128 + ((((lane >> 2) ^ (f1 & 7))) << 4) + ((lane & 3) << 2));
           if constexpr (kMode == kEpiRelu) {
             a0 = fmaxf(a0, 0.f);
             a1 = fmaxf(a1, 0.f);
@@ -275,35 +311,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           }
           packed[j] = pack_bf16x2(a0, a1);
         }
-        // stage [32 tokens][128 features] bf16, 16B chunks XOR-swizzled by token
+        // bf16 [token][32 features] rows of 64 B, chunk' = j ^ ((token/2)%4)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int chunk = (4 * q + j) ^ (lane & 15);
-          const uint32_t a = smem_u32(stg + lane * 256 + chunk * 16);
-          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(packed[4 * j]),
-                       "r"(packed[4 * j + 1]), "r"(packed[4 * j + 2]), "r"(packed[4 * j + 3])
-                       : "memory");
-        }
-        named_bar_sync(1, 128);
-        // cooperative stores: warp q writes token rows 8q..8q+7, 16 lanes x 16 B per row
+        for (int j = 0; j < 4; ++j)
+          sts128(sg + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4), packed[4 * j], packed[4 * j + 1],
+                 packed[4 * j + 2], packed[4 * j + 3]);
+        __syncwarp();
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const int r = 8 * q + 2 * i + (lane >> 4);
-          const int chunk = lane & 15;
+          const int r = 8 * i + (lane >> 2), j = lane & 3;
+          const uint4 x = lds128(sg + r * 64 + ((j ^ ((r >> 1) & 3)) << 4));
           const int tk = c + r;
-          const uint32_t a = smem_u32(stg + r * 256 + ((chunk ^ (r & 15)) << 4));
-          uint32_t x0, x1, x2, x3;
-          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                       : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3)
-                       : "r"(a));
           if (tk < t.ntok) {
             long dst;
             if constexpr (kMode == kEpiScaleScatter) dst = __ldg(p.row_token + row_base + tk);
             else dst = row_base + tk;
-            st_global_v4(p.out + dst * p.ldo + col0 + chunk * 8, x0, x1, x2, x3);
+            st_global_v4(p.out + dst * p.ldo + col0 + j * 8, x.x, x.y, x.z, x.w);
           }
         }
-        named_bar_sync(1, 128);
+        __syncwarp();
+      }
+      if (!released) {  // no chunk for this warp in a narrow tile
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(smem_u32(&tempty_bar[acc]) & kPeerMask);
       }
     }
   }
