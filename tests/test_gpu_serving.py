@@ -1,0 +1,67 @@
+"""Host-to-host pipeline and expert-parallel path on one GPU."""
+
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import switch_layer as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _layer(T, d, d_ff, E, seed=0):
+    from paper_2508_09208_b200 import ExpertPool, MoELayer, kernels
+    g = torch.Generator().manual_seed(seed)
+    x = torch.randn(T, d, generator=g).to(torch.bfloat16)
+    wg = (torch.randn(d, E, generator=g) / math.sqrt(d)).cuda()
+    numel = kernels.expert_numel(d, d_ff, kernels.ACT_RELU)
+    w = (torch.randn(E, numel, generator=g) * 0.02).to(torch.bfloat16)
+    pool = ExpertPool(E, numel)
+    pool.data[:, :numel].copy_(w.cuda())
+    return MoELayer(wg, pool, d_ff, capacity_factor=1.25), x, wg, w
+
+
+def test_host_pipeline_matches_device_forward():
+    from paper_2508_09208_b200.stream import HostPipeline
+    layer, x, wg, w = _layer(4096, 256, 512, 16)
+    xs = [(x + i).contiguous().pin_memory() for i in range(5)]
+    ys = [torch.empty_like(v).pin_memory() for v in xs]
+    pipe = HostPipeline(layer, 4096, 256)
+    pipe.run(xs, ys)
+    pipe.synchronize()
+    for xh, yh in zip(xs, ys):
+        ref = layer.forward(xh.cuda())
+        torch.cuda.synchronize()
+        assert torch.equal(yh, ref.cpu())
+
+
+def test_expert_parallel_world1_matches_oracle():
+    import torch.distributed as dist
+    from paper_2508_09208_b200.ep import EPMoELayer
+    from paper_2508_09208_b200.pool import ExpertPool
+    from paper_2508_09208_b200 import kernels
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", rank=0, world_size=1)
+    T, d, d_ff, E = 3000, 256, 512, 16
+    g = torch.Generator().manual_seed(4)
+    x = torch.randn(T, d, generator=g).to(torch.bfloat16)
+    wg = (torch.randn(d, E, generator=g) / math.sqrt(d)).cuda()
+    numel = kernels.expert_numel(d, d_ff, kernels.ACT_RELU)
+    w = (torch.randn(E, numel, generator=g) * 0.02).to(torch.bfloat16)
+    pool = ExpertPool(E, numel)
+    pool.data[:, :numel].copy_(w.cuda())
+    layer = EPMoELayer(wg, pool, d_ff, world=1, rank=0, capacity_factor=1.0)
+    y = layer.forward(x.cuda())
+    torch.cuda.synchronize()
+    logits = None
+    wi = np.stack([O.split_expert(w[e].float().numpy(), d, d_ff, "relu")[0] for e in range(E)])
+    wo = np.stack([O.split_expert(w[e].float().numpy(), d, d_ff, "relu")[1] for e in range(E)])
+    ref, info = O.layer_forward_fast(x.float().numpy(), wg.cpu().numpy(), wi, wo, 1, False, 1.0,
+                                     dtype=np.float64)
+    assert (info["pos"] < 0).sum() > 0
+    assert O.normwise_error(y.float().cpu().numpy(), ref) < 1e-2
