@@ -1,0 +1,312 @@
+"""HBM-budgeted expert cache (K7) and the MoE layer that runs on it.
+
+Every expert keeps a master copy in pinned host memory (weights are
+read-only, so the reference's CACHE->HOST eviction, simulator.py:480, is a
+free slot release). HBM holds `n_slots` expert slots (an ExpertPool). The
+residency decisions are the reference policy, unchanged
+(paper_2508_09208_b200.offload mirrors offload.py): tiers in a CacheState,
+popularity placement, hybrid eviction scores, threshold-gated prefetch and
+similarity substitution. Data movement is real: cudaMemcpyAsync (torch
+copy_) host->slot on a dedicated copy stream, one CUDA event per slot
+standing in for the simulator's `inflight[eid]` (simulator.py:617).
+
+CachedMoELayer.forward(x):
+  1. gate + capacity scan on the compute stream (as MoELayer);
+  2. one D2H of the per-group kept counts — the demand set (the only host
+     sync of the layer; the reference decides on the host too);
+  3. hits are served in place; misses are either substituted (slot of the
+     most similar resident expert, correct_misprediction) or fetched;
+  4. experts are processed in waves that fit the slot pool: wave k's grouped
+     GEMMs run while wave k+1's H2D copies stream into the other slots
+     (the compute stream waits per-slot events; the copy stream waits for
+     the GEMM event of the wave that last used a slot before overwriting it).
+Outputs are bit-identical to MoELayer.forward with every expert resident:
+the cache only changes where weights live, never the arithmetic.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import kernels
+from .errors import InfeasibleError
+from .layer import ACTS, MoELayer
+from .offload import (CACHE, HOST, WORKSPACE, CacheState, OffloadPolicy, build_cache_state,
+                      correct_misprediction, decide_prefetch, eviction_score, evict,
+                      plan_initial_placement)
+from .pool import ExpertPool
+
+
+@dataclass
+class CacheStats:
+    demand: int = 0
+    hits: int = 0
+    fetches: int = 0
+    prefetch_issued: int = 0
+    prefetch_hits: int = 0
+    substitutions: int = 0
+    evictions: int = 0
+    h2d_bytes: int = 0
+    waves: int = 0
+    events: list = field(default_factory=list)  # (kind, expert) in decision order
+
+    def hit_rate(self) -> float:
+        return self.hits / self.demand if self.demand else 0.0
+
+
+class ExpertCache:
+    """Slot manager + policy for one MoE layer's experts (ids (layer, slot))."""
+
+    def __init__(self, host_experts: torch.Tensor, layer: int, n_slots: int,
+                 workspace_slots: int = 2, policy: OffloadPolicy = None, freqs=None,
+                 pinned=(), device=None, substitution=False, similarity=None):
+        if not host_experts.is_pinned():
+            raise ValueError("host expert store must be pinned memory")
+        E, numel = host_experts.shape
+        if not 1 <= workspace_slots < n_slots:
+            raise ValueError("need 1 <= workspace_slots < n_slots")
+        self.host = host_experts
+        self.layer = layer
+        self.E = E
+        self.dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+        self.pool = ExpertPool(n_slots, numel, device=self.dev)
+        self.bytes = numel * host_experts.element_size()
+        self.policy = policy or OffloadPolicy()
+        self.substitution = substitution
+        self.similarity = similarity  # callable (eid_a, eid_b) -> float
+        self.copy_stream = torch.cuda.Stream(self.dev)
+        self.ready = [torch.cuda.Event() for _ in range(n_slots)]   # slot filled
+        self.free_ev = [torch.cuda.Event() for _ in range(n_slots)]  # slot's last reader done
+        self._free_pending = [False] * n_slots
+        self.slot_of = {}
+        self._free_slots = list(range(n_slots - 1, -1, -1))
+        self.stats = CacheStats()
+        self.tick = 0
+        self.last_probs = None
+        self.prefetched = set()
+        freqs = freqs if freqs is not None else {(layer, s): 1.0 / E for s in range(E)}
+        max_f = max(max(freqs.values()), 1e-12)
+        self.importance = {e: f / max_f for e, f in freqs.items()}
+        sizes = {(layer, s): float(self.bytes) for s in range(E)}
+        ws_cap = workspace_slots * float(self.bytes)
+        ca_cap = (n_slots - workspace_slots) * float(self.bytes)
+        plan = plan_initial_placement(sizes, freqs, ws_cap, ca_cap, pinned=frozenset(pinned),
+                                      working_set_bytes=float(self.bytes))
+        self.state = build_cache_state(plan, sizes, ws_cap, ca_cap, pinned=set(pinned),
+                                       importance=self.importance)
+        for eid in self.state.gpu_resident_ids():
+            self._load(eid)
+        self.hard_pinned = set(pinned)
+
+    # ------------------------------------------------------------ slots
+    def _load(self, eid):
+        slot = self._free_slots.pop()
+        self.slot_of[eid] = slot
+        with torch.cuda.stream(self.copy_stream):
+            if self._free_pending[slot]:
+                self.copy_stream.wait_event(self.free_ev[slot])
+            self.pool.view(slot).copy_(self.host[eid[1]], non_blocking=True)
+            self.ready[slot].record(self.copy_stream)
+        self.stats.h2d_bytes += self.bytes
+        return slot
+
+    def _release(self, eid):
+        slot = self.slot_of.pop(eid)
+        self._free_slots.append(slot)
+
+    def mark_used(self, slots, stream):
+        """Record that `stream` reads these slots (copies into them must wait)."""
+        for s in slots:
+            self.free_ev[s].record(stream)
+            self._free_pending[s] = True
+
+    def wait_ready(self, slots, stream):
+        for s in slots:
+            stream.wait_event(self.ready[s])
+
+    # ------------------------------------------------------------ policy
+    def _scores(self):
+        out = {}
+        probs = self.last_probs
+        for eid in self.state.cache:
+            if eid in self.state.pinned:
+                continue
+            p = float(probs[eid[1]]) if probs is not None else 0.0
+            out[eid] = eviction_score(p, self.state.recent_value(eid, self.tick),
+                                      self.importance.get(eid, 0.0), self.policy.delta_evict,
+                                      self.policy.lambda_evict)
+        return out
+
+    def _make_room_cache(self, nbytes) -> bool:
+        try:
+            victims = evict(self.state, nbytes, self._scores())
+        except InfeasibleError:
+            return False
+        for v in victims:
+            self.state.move(v, CACHE, HOST)
+            self._release(v)
+            self.prefetched.discard(v)
+            self.stats.evictions += 1
+            self.stats.events.append(("evict", v))
+        return True
+
+    def _room_in_workspace(self) -> bool:
+        """simulator._room_in_workspace (simulator.py:486-501) over a batch:
+        demote unpinned workspace entries FIFO to the cache (evicting cache
+        entries if needed, else to host). False when every workspace entry
+        belongs to the active (pinned) wave."""
+        b = float(self.bytes)
+        while self.state.free_bytes(WORKSPACE) < b:
+            victim = next((e for e in self.state.workspace if e not in self.state.pinned), None)
+            if victim is None:
+                return False
+            if self.state.free_bytes(CACHE) >= b or self._make_room_cache(b):
+                self.state.move(victim, WORKSPACE, CACHE)
+                self.stats.events.append(("demote", victim))
+            else:
+                self.state.move(victim, WORKSPACE, HOST)
+                self._release(victim)
+                self.stats.events.append(("evict", victim))
+        return True
+
+    def serve(self, demanded: list):
+        """Serve one wave of demanded expert ids (layer, slot), pinning each
+        so later misses of the same wave cannot evict it. Batched
+        generalisation of _serve_demand (simulator.py:517-574): a miss goes
+        to the workspace tier, or — when the workspace is full of this
+        wave's experts — to the cache tier. Returns {eid: pool slot} (the
+        substitute's slot for substituted experts)."""
+        out = {}
+        b = float(self.bytes)
+        for eid in demanded:
+            self.stats.demand += 1
+            if self.state.resident(eid):
+                self.stats.hits += 1
+                if eid in self.prefetched:
+                    self.stats.prefetch_hits += 1
+                    self.prefetched.discard(eid)
+                self.state.record_access(eid, self.tick)
+                self.state.pinned.add(eid)
+                out[eid] = self.slot_of[eid]
+                self.stats.events.append(("hit", eid))
+                continue
+            if self.substitution and self.similarity is not None:
+                dec = correct_misprediction(eid, self.state, self.similarity, self.policy,
+                                            priority=self.importance.get(eid, 0.0))
+                if dec.action == "substitute":
+                    self.stats.substitutions += 1
+                    self.state.record_access(dec.expert, self.tick)
+                    self.state.pinned.add(dec.expert)
+                    out[eid] = self.slot_of[dec.expert]
+                    self.stats.events.append(("substitute", eid))
+                    continue
+            if self._room_in_workspace():
+                tier = WORKSPACE
+            elif self.state.free_bytes(CACHE) >= b or self._make_room_cache(b):
+                tier = CACHE
+            else:
+                raise InfeasibleError("wave does not fit the HBM expert slots")
+            self.state.move(eid, HOST, tier)
+            self.state.pinned.add(eid)
+            self.state.record_access(eid, self.tick)
+            out[eid] = self._load(eid)
+            self.stats.fetches += 1
+            self.stats.events.append(("fetch", eid))
+        return out
+
+    def unpin(self, eids):
+        for e in eids:
+            if e not in self.hard_pinned:
+                self.state.pinned.discard(e)
+
+    def prefetch(self, probs, theta: float):
+        """Threshold-gated prefetch of next-use experts into the cache tier
+        (simulator._predict_and_prefetch, simulator.py:578-620); copies are
+        asynchronous on the copy stream."""
+        self.last_probs = np.asarray(probs, dtype=float)
+        chosen = decide_prefetch(self.last_probs, theta, self.state, self.layer,
+                                 lambda e: float(self.bytes))
+        for eid in chosen:
+            if self.state.free_bytes(CACHE) < self.bytes and not self._make_room_cache(self.bytes):
+                break
+            self.state.move(eid, HOST, CACHE)
+            self._load(eid)
+            self.prefetched.add(eid)
+            self.stats.prefetch_issued += 1
+            self.stats.events.append(("prefetch", eid))
+        return chosen
+
+    def check(self):
+        self.state.check_invariants()
+        assert len(self.slot_of) == len(self.state.workspace) + len(self.state.cache)
+        assert len(set(self.slot_of.values())) == len(self.slot_of)
+
+
+class CachedMoELayer:
+    """MoELayer whose experts live in an ExpertCache (Switch / top-1 or top-2)."""
+
+    def __init__(self, wg, cache: ExpertCache, d_ff: int, act="relu", top_k=1, norm_topk=None,
+                 capacity_factor=1.25, wave_slots: int = None):
+        self.cache = cache
+        self.E = cache.E
+        self.layer = MoELayer(wg, cache.pool, d_ff, act=act, top_k=top_k, norm_topk=norm_topk,
+                              capacity_factor=capacity_factor, expert_slots=[0] * cache.E)
+        free = cache.pool.n_slots - len(cache.hard_pinned)
+        # half the free slots per wave: wave k+1 can stream in while wave k computes
+        self.wave_slots = wave_slots or max(1, free // 2)
+        self._tables = torch.zeros((self.E, 2, self.E), dtype=torch.int32).pin_memory()
+        self._tables_dev = torch.zeros((self.E, 2, self.E), dtype=torch.int32, device=wg.device)
+
+    def forward(self, x, out=None):
+        L = self.layer
+        T = x.shape[0]
+        if out is None:
+            out = torch.empty((T, L.d), dtype=torch.bfloat16, device=x.device)
+        ws = L._workspace(T)
+        comp = torch.cuda.current_stream()
+        r = L.route(x)
+        k1 = L.top_k == 1
+        kernels.permute(x, r.gate, r.scan, r.capacity, r.rows, y_zero=out if k1 else None,
+                        out=r.perm)
+        kept = r.scan.group_kept.cpu().numpy()  # the demand set (the layer's one host sync)
+        c = self.cache
+        c.tick += 1
+        order = [int(g) for g in np.argsort(-kept, kind="stable") if kept[g] > 0]
+        hits = [g for g in order if c.state.resident((c.layer, g))]
+        misses = [g for g in order if not c.state.resident((c.layer, g))]
+        seq = hits + misses
+        waves = [seq[i:i + self.wave_slots] for i in range(0, len(seq), self.wave_slots)]
+        n1 = 2 * L.d_ff if L.act == "swiglu" else L.d_ff
+        dst = out if k1 else ws["y_perm"]
+        epi1 = kernels.EPI_SWIGLU if L.act == "swiglu" else kernels.EPI_RELU
+        epi2 = kernels.EPI_SCALE_SCATTER if k1 else kernels.EPI_STORE
+        tab = self._tables.numpy()
+        for w, wave in enumerate(waves):
+            ids = [(c.layer, g) for g in wave]
+            slots = c.serve(ids)
+            c.stats.waves += 1
+            tab[w] = 0
+            for g in wave:
+                tab[w, 0, g] = kept[g]
+                tab[w, 1, g] = slots[(c.layer, g)]
+            used = sorted({slots[e] for e in ids})
+            self._tables_dev[w].copy_(self._tables[w], non_blocking=True)
+            c.wait_ready(used, comp)
+            g_rows, g_slot = self._tables_dev[w, 0], self._tables_dev[w, 1]
+            kernels.grouped_gemm(r.perm.x_perm, c.pool.data, 0, n1, g_rows, r.scan.group_base,
+                                 g_slot, epi1, ws["h"])
+            kernels.grouped_gemm(ws["h"], c.pool.data, n1 * L.d, L.d, g_rows, r.scan.group_base,
+                                 g_slot, epi2, dst, row_token=r.perm.row_token if k1 else None,
+                                 row_prob=r.perm.row_prob if k1 else None)
+            c.mark_used(used, comp)
+            c.unpin(list(ids) + [e for e in c.slot_of if c.slot_of[e] in used])
+        if not k1:
+            kernels.combine(ws["y_perm"], r.perm.token_pos, r.gate.gate_prob, out=out)
+        c.check()
+        L.last = r
+        return out
+
+    __call__ = forward
