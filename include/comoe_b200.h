@@ -142,6 +142,9 @@ int comoe_merge(int dtype, const void* const* member_ptrs, const int* group_offs
  *   comoe_sim_workspace_bytes(E, n, B, D) bytes.
  * comoe_sim_finalize: S = alpha*cos + (1-alpha)*clip(1 - meanKL, 0, 1) with
  *   log-softmax surrogate distributions (finite where the reference NaNs).
+ * n_probes = 0 selects the cosine term only (probes/proj/logits may be NULL;
+ * the functional term is then the constant 1): real-scale experts (D ~ 1e8)
+ * where materialising the reference's n x D fp64 calibration is infeasible.
  */
 long comoe_sim_workspace_bytes(int E, int n_probes, int buckets, long D);
 int comoe_sim_contract(int dtype, const void* const* rows, int E, long D, const double* probes,

@@ -135,7 +135,7 @@ __global__ void sim_finalize_kernel(const double* __restrict__ gram,
       }
       mean_kl += 0.5 * (kab + kba);
     }
-    mean_kl /= n_probes;
+    if (n_probes > 0) mean_kl /= n_probes;
     double sf = 1.0 - mean_kl;
     sf = sf < 0.0 ? 0.0 : (sf > 1.0 ? 1.0 : sf);
     sim[idx] = alpha * cosv + (1.0 - alpha) * sf;
@@ -160,7 +160,7 @@ static int sim_splits(int E, int ncols, long D) {
 extern "C" {
 
 long comoe_sim_workspace_bytes(int E, int n_probes, int buckets, long D) {
-  const int ncols = E + n_probes * buckets;
+  const int ncols = E + (n_probes > 0 ? n_probes * buckets : 0);
   return static_cast<long>(comoe::sim_splits(E, ncols, D)) * E * ncols * sizeof(double);
 }
 
@@ -168,10 +168,11 @@ int comoe_sim_contract(int dtype, const void* const* rows, int E, long D, const 
                        int n_probes, const double* proj, int buckets, double* gram,
                        double* logits, void* work, void* stream) {
   using namespace comoe;
-  COMOE_REQUIRE(rows && probes && proj && gram && logits && work, kBadArg,
-                "sim_contract: null pointer");
-  COMOE_REQUIRE(E >= 1 && D >= 1 && n_probes >= 1 && buckets >= 1, kBadArg,
-                "sim_contract: bad sizes");
+  COMOE_REQUIRE(rows && gram && work, kBadArg, "sim_contract: null pointer");
+  COMOE_REQUIRE(n_probes == 0 || (probes && proj && logits && buckets >= 1), kBadArg,
+                "sim_contract: null calibration");
+  COMOE_REQUIRE(E >= 1 && D >= 1 && n_probes >= 0, kBadArg, "sim_contract: bad sizes");
+  if (n_probes == 0) buckets = 0;  // cosine only
   const int ncols = E + n_probes * buckets;
   const int splits = sim_splits(E, ncols, D);
   const int tiles_i = (E + kSimTile - 1) / kSimTile, tiles_j = (ncols + kSimTile - 1) / kSimTile;
@@ -199,7 +200,7 @@ int comoe_sim_contract(int dtype, const void* const* rows, int E, long D, const 
 int comoe_sim_finalize(const double* gram, const double* logits, int E, int n_probes, int buckets,
                        double alpha, double* sim, void* stream) {
   using namespace comoe;
-  COMOE_REQUIRE(gram && logits && sim, kBadArg, "sim_finalize: null pointer");
+  COMOE_REQUIRE(gram && sim && (logits || n_probes == 0), kBadArg, "sim_finalize: null pointer");
   COMOE_REQUIRE(alpha >= 0.0 && alpha <= 1.0, kBadArg, "sim_finalize: alpha=%g", alpha);
   const long pairs = static_cast<long>(E) * E;
   const int blocks = static_cast<int>((pairs + 127) / 128 < 1024 ? (pairs + 127) / 128 : 1024);

@@ -281,17 +281,21 @@ def similarity(rows, probes, proj, alpha):
         _need(r, "row", dt, align=r.element_size())
         if r.numel() != D:
             raise ValueError("parameter dimension mismatch")
-    _need(probes, "probes", torch.float64, 2)
-    _need(proj, "proj", torch.float64, 2)
-    n, B = probes.shape[0], proj.shape[0]
-    if probes.shape[1] != D or proj.shape[1] != D:
-        raise ValueError("calibration dimension mismatch")
+    n = 0 if probes is None else probes.shape[0]
+    B = 0 if proj is None else proj.shape[0]
+    if n:
+        _need(probes, "probes", torch.float64, 2)
+        _need(proj, "proj", torch.float64, 2)
+        if probes.shape[1] != D or proj.shape[1] != D:
+            raise ValueError("calibration dimension mismatch")
+    else:
+        probes = proj = None
     dev = rows[0].device
     t_rows = torch.tensor([r.data_ptr() for r in rows], dtype=torch.int64).to(dev)
     ws = _lib.load().comoe_sim_workspace_bytes(E, n, B, D)
     work = torch.empty(max(ws, 8), dtype=torch.uint8, device=dev)
     gram = torch.empty((E, E), dtype=torch.float64, device=dev)
-    logits = torch.empty((E, n, B), dtype=torch.float64, device=dev)
+    logits = torch.empty((E, n, B), dtype=torch.float64, device=dev) if n else None
     sim = torch.empty((E, E), dtype=torch.float64, device=dev)
     code = DTYPE_BF16 if dt == torch.bfloat16 else DTYPE_F64
     _lib.call("comoe_sim_contract", code, _ptr(t_rows), E, D, _ptr(probes), n, _ptr(proj), B,

@@ -152,12 +152,22 @@ class Calibration:
     projection: np.ndarray  # (buckets, dim)
 
     def device(self, device="cuda"):
+        if self.probes is None or len(self.probes) == 0:
+            return None, None  # cosine-only calibration
         key = ("dev", str(device))
         cache = self.__dict__.setdefault("_dev_cache", {})
         if key not in cache:
             cache[key] = (torch.as_tensor(np.ascontiguousarray(self.probes, np.float64), device=device),
                           torch.as_tensor(np.ascontiguousarray(self.projection, np.float64), device=device))
         return cache[key]
+
+
+def cosine_only_calibration() -> Calibration:
+    """Calibration with no probes: similarity_matrix then returns
+    alpha*cos + (1-alpha) (the functional term is the constant 1). For
+    real-scale experts, where the reference's n x D fp64 probe/projection
+    matrices would not fit in memory."""
+    return Calibration(probes=None, projection=None)
 
 
 def make_calibration(dim: int, n_probes: int = 8, seed: int = 7, buckets: int = 8) -> Calibration:
