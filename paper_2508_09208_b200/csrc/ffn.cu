@@ -27,20 +27,41 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const Group
   return check_launch("grouped_gemm_kernel");
 }
 
-template <int kMode>
-static int launch_gemm_2sm(const CUtensorMap& tw, const CUtensorMap& tx,
-                           const GroupedGemmParams& p, cudaStream_t stream) {
-  auto kern = grouped_gemm_2sm_kernel<kMode>;
+template <int kMode, int kStages, int kEpiWarps>
+static int launch_gemm_2sm_cfg(const CUtensorMap& tw, const CUtensorMap& tx,
+                               const GroupedGemmParams& p, cudaStream_t stream) {
+  using C = Gemm2Cfg<kStages, kEpiWarps>;
+  auto kern = grouped_gemm_2sm_kernel<kMode, kStages, kEpiWarps>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Gemm2Smem::kTotal);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kTotal);
     attr_set = true;
   }
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  kern<<<sms & ~1, k2Threads, Gemm2Smem::kTotal, stream>>>(tw, tx, p);
+  kern<<<sms & ~1, C::kThreads, C::kTotal, stream>>>(tw, tx, p);
   return check_launch("grouped_gemm_2sm_kernel");
+}
+
+// pipeline config (COMOE_GEMM2_CFG=0..2 for A/B runs): 0 = 5 stages x 8 epilogue
+// warps, 1 = 4 x 8, 2 = 6 x 4
+static int gemm2_cfg() {
+  static const int c = [] {
+    const char* e = std::getenv("COMOE_GEMM2_CFG");
+    return e ? std::atoi(e) : 0;
+  }();
+  return c;
+}
+
+template <int kMode>
+static int launch_gemm_2sm(const CUtensorMap& tw, const CUtensorMap& tx,
+                           const GroupedGemmParams& p, cudaStream_t stream) {
+  switch (gemm2_cfg()) {
+    case 1: return launch_gemm_2sm_cfg<kMode, 4, 8>(tw, tx, p, stream);
+    case 2: return launch_gemm_2sm_cfg<kMode, 6, 4>(tw, tx, p, stream);
+    default: return launch_gemm_2sm_cfg<kMode, 5, 8>(tw, tx, p, stream);
+  }
 }
 
 static bool force_1sm() {
@@ -77,6 +98,7 @@ static int grouped_gemm_impl(const void* a, long a_rows, const void* pool, int n
                       reinterpret_cast<__nv_bfloat16*>(out), ldo, row_token, row_prob};
   int rc;
   if (epi_mode != kEpiSwiGLU && !force_1sm()) {
+    COMOE_REQUIRE(G <= kMaxGroups2, kBadArg, "grouped_gemm: G=%d > %d", G, kMaxGroups2);
     // 2-SM swap-AB kernel: weights = A (128-feature boxes), tokens = B (128-row boxes)
     rc = make_tmap_bf16_3d(&tb, b, n_slots, N, K, slot_stride, 128);
     if (rc) return rc;

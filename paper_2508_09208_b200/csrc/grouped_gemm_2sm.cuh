@@ -21,19 +21,23 @@ namespace comoe {
 constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // clear the peer-CTA bit -> leader's smem
 constexpr int k2BM = 256;                    // features per CTA pair
 constexpr int k2BN = 256;                    // max tokens per tile
-constexpr int k2Stages = 4;
-constexpr int k2EpiWarps = 8;                     // 2 per TMEM lane quarter
-constexpr int k2Threads = 128 + 32 * k2EpiWarps;  // w0 TMA, w1 MMA, w2 TMEM, w3 idle, w4.. epilogue
+constexpr int kMaxGroups2 = 1024;
+constexpr int k2MaxThreads = 128 + 32 * 8;
 
-struct Gemm2Smem {
-  static constexpr int kABytes = 128 * kGemmBK * 2;  // 128 feature rows x 64 K
-  static constexpr int kBBytes = 128 * kGemmBK * 2;  // up to 128 token rows x 64 K
+// kStages: smem pipeline depth (32 KB per stage per SM); kEpiWarps: 4 or 8
+// epilogue warps (1 or 2 per TMEM lane quarter).
+template <int kStages, int kEpiWarps>
+struct Gemm2Cfg {
+  static constexpr int kThreads = 128 + 32 * kEpiWarps;  // w0 TMA, w1 MMA, w2 TMEM, w3 idle
+  static constexpr int kABytes = 128 * kGemmBK * 2;     // 128 feature rows x 64 K
+  static constexpr int kBBytes = 128 * kGemmBK * 2;     // up to 128 token rows x 64 K
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kTileBytes = k2Stages * kStageBytes;
-  static constexpr int kXposeBytes = k2EpiWarps * 32 * 32 * 4;  // per-warp fp32 32x32 transpose
-  static constexpr int kStgBytes = k2EpiWarps * 32 * 64;        // per-warp 32 tokens x 32 features bf16
-  static constexpr int kCtrlBytes = (2 * k2Stages + 4) * 8 + 16 + (kMaxGroups + 1) * 4;
+  static constexpr int kTileBytes = kStages * kStageBytes;
+  static constexpr int kXposeBytes = kEpiWarps * 32 * 32 * 4;  // per-warp fp32 32x32 transpose
+  static constexpr int kStgBytes = kEpiWarps * 32 * 64;        // per-warp 32 tokens x 32 feats
+  static constexpr int kCtrlBytes = (2 * kStages + 4) * 8 + 16 + (kMaxGroups2 + 1) * 4;
   static constexpr int kTotal = 1024 + kTileBytes + kXposeBytes + kStgBytes + kCtrlBytes;
+  static_assert(kTotal <= 227 * 1024, "shared memory");
 };
 
 __device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
@@ -100,9 +104,10 @@ __device__ __forceinline__ void umma_commit_2sm_mc(uint64_t* bar) {
 // tiles of a group: ceil(rows/256) token tiles x (N/256) feature tiles
 __device__ __forceinline__ void build_tile_prefix_2sm(const int* __restrict__ rows, int G,
                                                       int f_tiles, int* prefix) {
-  __shared__ int warp_tot2[k2Threads / 32];
+  __shared__ int warp_tot2[k2MaxThreads / 32];
   const int tid = threadIdx.x;
-  const int per = (G + k2Threads - 1) / k2Threads;
+  const int nthreads = blockDim.x;
+  const int per = (G + nthreads - 1) / nthreads;
   const int g0 = tid * per;
   int local = 0;
   for (int i = 0; i < per; ++i)
@@ -125,7 +130,7 @@ __device__ __forceinline__ void build_tile_prefix_2sm(const int* __restrict__ ro
       run += ((__ldg(rows + g) + k2BN - 1) / k2BN) * f_tiles;
     }
   }
-  if (tid == k2Threads - 1) prefix[G] = run;
+  if (tid == nthreads - 1) prefix[G] = run;
   __syncthreads();
 }
 
@@ -147,12 +152,12 @@ __device__ __forceinline__ Tile2 decode_tile2(const int* prefix, const GroupedGe
   return t;
 }
 
-template <int kMode>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k2Threads, 1)
+template <int kMode, int k2Stages, int k2EpiWarps>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k2EpiWarps>::kThreads, 1)
     grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmap_w,
                             const __grid_constant__ CUtensorMap tmap_x, GroupedGemmParams p) {
   static_assert(kMode != kEpiSwiGLU, "SwiGLU uses the 1-SM kernel");
-  using S = Gemm2Smem;
+  using S = Gemm2Cfg<k2Stages, k2EpiWarps>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -262,6 +267,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k2Threads, 1)
     // layouts are XOR-swizzled on 16-byte chunks: conflict-free both ways.
     const int ew = warp - 4;
     const int q = warp & 3, sub = ew >> 2;
+    constexpr int kSubs = k2EpiWarps / 4;
     const uint32_t xp = smem_u32(xpose) + ew * (32 * 32 * 4);
     const uint32_t sg = smem_u32(stg) + ew * (32 * 64);
     int it = 0;
@@ -275,12 +281,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k2Threads, 1)
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * k2BN;
       const int chunks = (t.nmma + 31) >> 5;
       bool released = false;
-      for (int ci = sub; ci < chunks; ci += 2) {
+      for (int ci = sub; ci < chunks; ci += kSubs) {
         const int c = ci * 32;
         uint32_t v[32];
         tmem_ld32(t_row + c, v);
         tmem_ld_wait();
-        if (ci + 2 >= chunks) {  // this warp's last TMEM read of the tile
+        if (ci + kSubs >= chunks) {  // this warp's last TMEM read of the tile
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(smem_u32(&tempty_bar[acc]) & kPeerMask);
