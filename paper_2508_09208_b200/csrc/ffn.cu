@@ -44,8 +44,8 @@ static int launch_gemm_2sm_cfg(const CUtensorMap& tw, const CUtensorMap& tx,
   return check_launch("grouped_gemm_2sm_kernel");
 }
 
-// pipeline config (COMOE_GEMM2_CFG=0..2 for A/B runs): 0 = 5 stages x 8 epilogue
-// warps, 1 = 4 x 8, 2 = 6 x 4
+// pipeline config (COMOE_GEMM2_CFG=0..3 for A/B runs): 0 = 6 stages x 8 epilogue
+// warps, 1 = 4 x 8, 2 = 6 x 4, 3 = 5 x 8
 static int gemm2_cfg() {
   static const int c = [] {
     const char* e = std::getenv("COMOE_GEMM2_CFG");
@@ -60,8 +60,17 @@ static int launch_gemm_2sm(const CUtensorMap& tw, const CUtensorMap& tx,
   switch (gemm2_cfg()) {
     case 1: return launch_gemm_2sm_cfg<kMode, 4, 8>(tw, tx, p, stream);
     case 2: return launch_gemm_2sm_cfg<kMode, 6, 4>(tw, tx, p, stream);
-    default: return launch_gemm_2sm_cfg<kMode, 5, 8>(tw, tx, p, stream);
+    case 3: return launch_gemm_2sm_cfg<kMode, 5, 8>(tw, tx, p, stream);
+    default: return launch_gemm_2sm_cfg<kMode, 6, 8>(tw, tx, p, stream);
   }
+}
+
+static int gemm_debug() {
+  static const int d = [] {
+    const char* e = std::getenv("COMOE_GEMM_DEBUG");
+    return e ? std::atoi(e) : 0;
+  }();
+  return d;
 }
 
 static bool force_1sm() {
@@ -95,7 +104,8 @@ static int grouped_gemm_impl(const void* a, long a_rows, const void* pool, int n
   CUtensorMap ta, tb;
   const void* b = static_cast<const __nv_bfloat16*>(pool) + b_offset;
   GroupedGemmParams p{group_rows, group_row_base, group_slot, G, N, K,
-                      reinterpret_cast<__nv_bfloat16*>(out), ldo, row_token, row_prob};
+                      reinterpret_cast<__nv_bfloat16*>(out), ldo, row_token, row_prob,
+                      gemm_debug()};
   int rc;
   if (epi_mode != kEpiSwiGLU && !force_1sm()) {
     COMOE_REQUIRE(G <= kMaxGroups2, kBadArg, "grouped_gemm: G=%d > %d", G, kMaxGroups2);

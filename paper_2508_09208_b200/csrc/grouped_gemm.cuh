@@ -36,6 +36,8 @@ struct GroupedGemmParams {
   int ldo;  // elements
   const int* row_token;   // kEpiScaleScatter
   const float* row_prob;  // kEpiScaleScatter
+  int debug;              // dev-only attribution switches (COMOE_GEMM_DEBUG): 1 = no epilogue
+                          // math/stores, 2 = no TMA (MMA on stale smem); 0 in production
 };
 
 constexpr int kGemmBM = 128;

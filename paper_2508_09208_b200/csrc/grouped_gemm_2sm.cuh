@@ -33,7 +33,7 @@ struct Gemm2Cfg {
   static constexpr int kBBytes = 128 * kGemmBK * 2;     // up to 128 token rows x 64 K
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTileBytes = kStages * kStageBytes;
-  static constexpr int kXposeBytes = kEpiWarps * 32 * 32 * 4;  // per-warp fp32 32x32 transpose
+  static constexpr int kXposeBytes = 0;                          // (register transpose)
   static constexpr int kStgBytes = kEpiWarps * 32 * 64;        // per-warp 32 tokens x 32 feats
   static constexpr int kCtrlBytes = (2 * kStages + 4) * 8 + 16 + (kMaxGroups2 + 1) * 4;
   static constexpr int kTotal = 1024 + kTileBytes + kXposeBytes + kStgBytes + kCtrlBytes;
@@ -223,10 +223,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k
         for (int kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           const uint32_t fb = smem_u32(&full_bar[stage]) & kPeerMask;
-          if (leader) mbar_expect_tx(&full_bar[stage], 2 * S::kStageBytes);
-          else mbar_arrive_cluster(fb);
-          tma_load_3d_2sm(smem_a + stage * S::kABytes, &tmap_w, fb, kb * kGemmBK, feat, slot, pol_w);
-          tma_load_2d_2sm(smem_b + stage * S::kBBytes, &tmap_x, fb, kb * kGemmBK, tok, pol_x);
+          if (p.debug & 2) {  // dev: no data movement
+            if (leader) mbar_arrive(&full_bar[stage]);
+            else mbar_arrive_cluster(fb);
+          } else {
+            if (leader) mbar_expect_tx(&full_bar[stage], 2 * S::kStageBytes);
+            else mbar_arrive_cluster(fb);
+            tma_load_3d_2sm(smem_a + stage * S::kABytes, &tmap_w, fb, kb * kGemmBK, feat, slot, pol_w);
+            tma_load_2d_2sm(smem_b + stage * S::kBBytes, &tmap_x, fb, kb * kGemmBK, tok, pol_x);
+          }
           if (++stage == k2Stages) { stage = 0; phase ^= 1; }
         }
       }
@@ -268,7 +273,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k
     const int ew = warp - 4;
     const int q = warp & 3, sub = ew >> 2;
     constexpr int kSubs = k2EpiWarps / 4;
-    const uint32_t xp = smem_u32(xpose) + ew * (32 * 32 * 4);
     const uint32_t sg = smem_u32(stg) + ew * (32 * 64);
     int it = 0;
     for (int tile = cluster; tile < total_tiles; tile += n_clusters, ++it) {
@@ -292,41 +296,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k
           if (lane == 0) mbar_arrive_cluster(smem_u32(&tempty_bar[acc]) & kPeerMask);
           released = true;
         }
-        // fp32 [feature][token] with chunk' = (token/4) ^ (feature%8)
+        if (p.debug & 1) continue;  // dev: TMEM read only
+        // epilogue math in the feature-major registers: v[j] = D[feature lane][token c+j]
+        if constexpr (kMode == kEpiRelu) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          sts128(xp + lane * 128 + ((j ^ (lane & 7)) << 4), v[4 * j], v[4 * j + 1], v[4 * j + 2],
-                 v[4 * j + 3]);
-        __syncwarp();
-        const int tok = c + lane;  // this thread now owns token `tok`
-        float scale = 1.f;
-        if constexpr (kMode == kEpiScaleScatter)
-          scale = tok < t.ntok ? __ldg(p.row_prob + row_base + tok) : 0.f;
-        uint32_t packed[16];
+          for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(fmaxf(__uint_as_float(v[j]), 0.f));
+        } else if constexpr (kMode == kEpiScaleScatter) {
+          const float my_p = (c + lane < t.ntok) ? __ldg(p.row_prob + row_base + c + lane) : 0.f;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            v[j] = __float_as_uint(__uint_as_float(v[j]) * __shfl_sync(0xffffffffu, my_p, j));
+        }
+        // register transpose of feature pairs: lane 2p keeps tokens 0..15, lane 2p+1
+        // tokens 16..31; one shfl_xor per token swaps the partner feature in
+        const bool odd = lane & 1;
+        const uint32_t prow = static_cast<uint32_t>(lane >> 1);  // feature pair index
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          const int f0 = 2 * j, f1 = 2 * j + 1;
-          float a0 = lds_f32(xp + f0 * 128 + ((((lane >> 2) ^ (f0 & 7))) << 4) + ((lane & 3) << 2));
-          float a1 = lds_f32(xp + f1 * 128 + ((((lane >> 2) ^ (f1 & 7))) << 4) + ((lane & 3) << 2));
-          if constexpr (kMode == kEpiRelu) {
-            a0 = fmaxf(a0, 0.f);
-            a1 = fmaxf(a1, 0.f);
-          } else if constexpr (kMode == kEpiScaleScatter) {
-            a0 *= scale;
-            a1 *= scale;
-          }
-          packed[j] = pack_bf16x2(a0, a1);
+          const float send = __uint_as_float(odd ? v[j] : v[16 + j]);
+          const float recv = __shfl_xor_sync(0xffffffffu, send, 1);
+          const float lo = odd ? recv : __uint_as_float(v[j]);        // feature 2p
+          const float hi = odd ? __uint_as_float(v[16 + j]) : recv;   // feature 2p+1
+          const int tok_r = odd ? 16 + j : j;                          // staging row
+          // bf16 [32 tokens][32 features] rows of 64 B; word p ^ 8 in the upper 16 rows
+          // keeps the even/odd halves of the warp on different banks
+          const uint32_t word = prow ^ ((tok_r >> 4) << 3);
+          asm volatile("st.shared.b32 [%0], %1;" ::"r"(sg + tok_r * 64 + word * 4),
+                       "r"(pack_bf16x2(lo, hi))
+                       : "memory");
         }
-        // bf16 [token][32 features] rows of 64 B, chunk' = j ^ ((token/2)%4)
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          sts128(sg + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4), packed[4 * j], packed[4 * j + 1],
-                 packed[4 * j + 2], packed[4 * j + 3]);
         __syncwarp();
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int r = 8 * i + (lane >> 2), j = lane & 3;
-          const uint4 x = lds128(sg + r * 64 + ((j ^ ((r >> 1) & 3)) << 4));
+          const uint4 x = lds128(sg + r * 64 + ((j ^ ((r >> 4) << 1)) << 4));
           const int tk = c + r;
           if (tk < t.ntok) {
             long dst;
