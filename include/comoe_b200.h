@@ -87,7 +87,8 @@ int comoe_expert_histogram(const int* expert_idx, long n, int E, int* counts, vo
  * Kept assignments are copied to x_perm[group_base[g] + rank] (expert-sorted,
  * compact); row_token/row_prob describe each row; token_pos[T,k] = row or -1.
  * If y_zero != NULL, rows of tokens with no kept assignment are zeroed there
- * (the top-1 fused-combine output).
+ * (the top-1 fused-combine output). x_perm == NULL computes the routing
+ * tables only (the GEMM then gathers token rows itself, see a_gather).
  */
 int comoe_permute(const void* x, int T, int d, int top_k, const int* group_idx,
                   const float* gate_prob, const int* local_rank, const int* tile_offset,
@@ -104,12 +105,16 @@ int comoe_permute(const void* x, int T, int d, int top_k, const int* group_idx,
  * given, the second GEMM scales by row_prob and scatters rows to
  * out[row_token[r]] (fused top-1 combine); otherwise it stores rows in place.
  * Requires d, d_ff multiples of 256 and of 64.
+ * comoe_grouped_gemm: one GEMM of the pair; if a_gather != NULL, row r of
+ * group g of the token operand is row a_gather[group_row_base[g] + r] of `a`
+ * (TMA gather4 straight from the unpermuted tokens — no permuted copy; ReLU
+ * epilogue only). Outputs stay in the compact row order.
  */
 int comoe_grouped_gemm(const void* a, long a_rows, const void* pool, int n_slots, long slot_stride,
                        long b_offset, int N, int K, const int* group_rows,
                        const int* group_row_base, const int* group_slot, int G, int epi_mode,
                        void* out, int ldo, const int* row_token, const float* row_prob,
-                       void* stream);
+                       const int* a_gather, void* stream);
 int comoe_grouped_ffn(const void* x_perm, long total_rows, int d, int d_ff, int act,
                       const void* pool, int n_slots, long slot_stride, const int* group_rows,
                       const int* group_row_base, const int* group_slot, int G, void* h_work,

@@ -33,7 +33,7 @@ _SIGNATURES = {
     "comoe_permute": [_p, _c_int, _c_int, _c_int, _p, _p, _p, _p, _p, _c_int, _c_int, _p,
                       _p, _p, _p, _p, _p],
     "comoe_grouped_gemm": [_p, _c_long, _p, _c_int, _c_long, _c_long, _c_int, _c_int, _p, _p,
-                           _p, _c_int, _c_int, _p, _c_int, _p, _p, _p],
+                           _p, _c_int, _c_int, _p, _c_int, _p, _p, _p, _p],
     "comoe_grouped_ffn": [_p, _c_long, _c_int, _c_int, _c_int, _p, _c_int, _c_long, _p, _p,
                           _p, _c_int, _p, _p, _c_int, _p, _p, _p],
     "comoe_combine": [_p, _p, _p, _c_int, _c_int, _c_int, _p, _p],

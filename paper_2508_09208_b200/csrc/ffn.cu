@@ -31,6 +31,23 @@ template <int kMode, int kStages, int kEpiWarps>
 static int launch_gemm_2sm_cfg(const CUtensorMap& tw, const CUtensorMap& tx,
                                const GroupedGemmParams& p, cudaStream_t stream) {
   using C = Gemm2Cfg<kStages, kEpiWarps>;
+  if (p.gather_rows) {
+    if constexpr (kMode == kEpiRelu) {
+      auto kg = grouped_gemm_2sm_kernel<kMode, kStages, kEpiWarps, true>;
+      static bool attr_g = false;
+      if (!attr_g) {
+        cudaFuncSetAttribute(kg, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kTotal);
+        attr_g = true;
+      }
+      int dev = 0, sms = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      kg<<<sms & ~1, C::kThreads, C::kTotal, stream>>>(tw, tx, p);
+      return check_launch("grouped_gemm_2sm_kernel(gather)");
+    }
+    set_error("grouped_gemm: row gather is only supported with the ReLU epilogue");
+    return kUnsupportedShape;
+  }
   auto kern = grouped_gemm_2sm_kernel<kMode, kStages, kEpiWarps>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -86,7 +103,8 @@ static int grouped_gemm_impl(const void* a, long a_rows, const void* pool, int n
                              long slot_stride, long b_offset, int N, int K,
                              const int* group_rows, const int* group_row_base,
                              const int* group_slot, int G, int epi_mode, void* out, int ldo,
-                             const int* row_token, const float* row_prob, cudaStream_t stream) {
+                             const int* row_token, const float* row_prob, cudaStream_t stream,
+                             const int* a_gather = nullptr) {
   COMOE_REQUIRE(a && pool && out && group_rows && group_row_base && group_slot, kBadArg,
                 "grouped_gemm: null pointer");
   COMOE_REQUIRE(G >= 1 && G <= kMaxGroups, kBadArg, "grouped_gemm: G=%d out of [1,%d]", G,
@@ -105,14 +123,14 @@ static int grouped_gemm_impl(const void* a, long a_rows, const void* pool, int n
   const void* b = static_cast<const __nv_bfloat16*>(pool) + b_offset;
   GroupedGemmParams p{group_rows, group_row_base, group_slot, G, N, K,
                       reinterpret_cast<__nv_bfloat16*>(out), ldo, row_token, row_prob,
-                      gemm_debug()};
+                      a_gather, gemm_debug()};
   int rc;
   if (epi_mode != kEpiSwiGLU && !force_1sm()) {
     COMOE_REQUIRE(G <= kMaxGroups2, kBadArg, "grouped_gemm: G=%d > %d", G, kMaxGroups2);
     // 2-SM swap-AB kernel: weights = A (128-feature boxes), tokens = B (128-row boxes)
     rc = make_tmap_bf16_3d(&tb, b, n_slots, N, K, slot_stride, 128);
     if (rc) return rc;
-    rc = make_tmap_bf16_2d(&ta, a, static_cast<uint64_t>(a_rows), K, 128);
+    rc = make_tmap_bf16_2d(&ta, a, static_cast<uint64_t>(a_rows), K, a_gather ? 1 : 128);
     if (rc) return rc;
     switch (epi_mode) {
       case kEpiRelu: return launch_gemm_2sm<kEpiRelu>(tb, ta, p, stream);
@@ -123,6 +141,8 @@ static int grouped_gemm_impl(const void* a, long a_rows, const void* pool, int n
     set_error("grouped_gemm: unknown epilogue mode %d", epi_mode);
     return kBadArg;
   }
+  COMOE_REQUIRE(a_gather == nullptr, kUnsupportedShape,
+                "grouped_gemm: row gather needs the 2-SM kernel (not SwiGLU / COMOE_GEMM_1SM)");
   rc = make_tmap_bf16_2d(&ta, a, static_cast<uint64_t>(a_rows), K, kGemmBM);
   if (rc) return rc;
   rc = make_tmap_bf16_3d(&tb, b, n_slots, N, K, slot_stride, 256);
@@ -146,10 +166,11 @@ int comoe_grouped_gemm(const void* a, long a_rows, const void* pool, int n_slots
                        long b_offset, int N, int K, const int* group_rows,
                        const int* group_row_base, const int* group_slot, int G, int epi_mode,
                        void* out, int ldo, const int* row_token, const float* row_prob,
-                       void* stream) {
+                       const int* a_gather, void* stream) {
   return comoe::grouped_gemm_impl(a, a_rows, pool, n_slots, slot_stride, b_offset, N, K,
                                   group_rows, group_row_base, group_slot, G, epi_mode, out, ldo,
-                                  row_token, row_prob, static_cast<cudaStream_t>(stream));
+                                  row_token, row_prob, static_cast<cudaStream_t>(stream),
+                                  a_gather);
 }
 
 int comoe_grouped_ffn(const void* x_perm, long total_rows, int d, int d_ff, int act,

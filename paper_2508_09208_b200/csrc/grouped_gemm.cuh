@@ -36,6 +36,8 @@ struct GroupedGemmParams {
   int ldo;  // elements
   const int* row_token;   // kEpiScaleScatter
   const float* row_prob;  // kEpiScaleScatter
+  const int* gather_rows; // 2-SM kernel: B-operand row r of group g is row
+                          // gather_rows[row_base[g] + r] of the token tensor (TMA gather4)
   int debug;              // dev-only attribution switches (COMOE_GEMM_DEBUG): 1 = no epilogue
                           // math/stores, 2 = no TMA (MMA on stale smem); 0 in production
 };

@@ -85,6 +85,18 @@ __device__ __forceinline__ void tma_load_3d_2sm(void* dst, const CUtensorMap* ma
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y), "r"(z), "l"(policy)
       : "memory");
 }
+// 4 token rows (box {64 cols, 1 row}) into 512 contiguous smem bytes; the
+// transaction completes on the pair leader's mbarrier (peer-masked address)
+__device__ __forceinline__ void tma_gather4_2sm(void* dst, const CUtensorMap* map, uint32_t bar,
+                                                int32_t x, int r0, int r1, int r2, int r3,
+                                                uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+      ".cta_group::2.L2::cache_hint [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
+      "l"(policy)
+      : "memory");
+}
 __device__ __forceinline__ void umma_bf16_2sm(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                               uint32_t idesc, uint32_t accumulate) {
   asm volatile(
@@ -152,7 +164,7 @@ __device__ __forceinline__ Tile2 decode_tile2(const int* prefix, const GroupedGe
   return t;
 }
 
-template <int kMode, int k2Stages, int k2EpiWarps>
+template <int kMode, int k2Stages, int k2EpiWarps, bool kGather = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k2EpiWarps>::kThreads, 1)
     grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmap_w,
                             const __grid_constant__ CUtensorMap tmap_x, GroupedGemmParams p) {
@@ -208,21 +220,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k
 
   if (warp == 0) {
     // ---------------------------------------------- TMA producer (both CTAs)
-    if (elect_one()) {
-      const uint64_t pol_w = l2_policy_evict_last();
-      // token rows are re-read by every feature tile of the group: keep them
-      // (evict_first here doubled DRAM reads of H, profiles/r1_2sm_evict_first)
-      const uint64_t pol_x = l2_policy_evict_last();
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int tile = cluster; tile < total_tiles; tile += n_clusters) {
-        const Tile2 t = decode_tile2(prefix, p, f_tiles, tile);
-        const int slot = __ldg(p.group_slot + t.g);
-        const int feat = t.ft * k2BM + static_cast<int>(rank) * 128;
-        const int tok = __ldg(p.group_row_base + t.g) + t.tok0 + static_cast<int>(rank) * (t.nmma >> 1);
-        for (int kb = 0; kb < k_blocks; ++kb) {
+    const uint64_t pol_w = l2_policy_evict_last();
+    // token rows are re-read by every feature tile of the group: keep them
+    // (evict_first here doubled DRAM reads of H, profiles/r1_2sm_evict_first)
+    const uint64_t pol_x = l2_policy_evict_last();
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = cluster; tile < total_tiles; tile += n_clusters) {
+      const Tile2 t = decode_tile2(prefix, p, f_tiles, tile);
+      const int slot = __ldg(p.group_slot + t.g);
+      const int feat = t.ft * k2BM + static_cast<int>(rank) * 128;
+      const int gbase = __ldg(p.group_row_base + t.g);
+      const int half0 = t.tok0 + static_cast<int>(rank) * (t.nmma >> 1);
+      int idx0 = 0, idx1 = 0, idx2 = 0, idx3 = 0;
+      if constexpr (kGather) {
+        // this lane gathers rows 4*lane .. 4*lane+3 of the CTA's token half
+        // (padding rows point at the group's first token; their columns are dropped)
+        int rr[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r = half0 + 4 * lane + i;
+          rr[i] = __ldg(p.gather_rows + gbase + (r < t.tok0 + t.ntok ? r : t.tok0));
+        }
+        idx0 = rr[0]; idx1 = rr[1]; idx2 = rr[2]; idx3 = rr[3];
+      }
+      for (int kb = 0; kb < k_blocks; ++kb) {
+        const uint32_t fb = smem_u32(&full_bar[stage]) & kPeerMask;
+        if (lane == 0) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
-          const uint32_t fb = smem_u32(&full_bar[stage]) & kPeerMask;
           if (p.debug & 2) {  // dev: no data movement
             if (leader) mbar_arrive(&full_bar[stage]);
             else mbar_arrive_cluster(fb);
@@ -230,10 +255,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k
             if (leader) mbar_expect_tx(&full_bar[stage], 2 * S::kStageBytes);
             else mbar_arrive_cluster(fb);
             tma_load_3d_2sm(smem_a + stage * S::kABytes, &tmap_w, fb, kb * kGemmBK, feat, slot, pol_w);
-            tma_load_2d_2sm(smem_b + stage * S::kBBytes, &tmap_x, fb, kb * kGemmBK, tok, pol_x);
+            if constexpr (!kGather)
+              tma_load_2d_2sm(smem_b + stage * S::kBBytes, &tmap_x, fb, kb * kGemmBK,
+                              gbase + half0, pol_x);
           }
-          if (++stage == k2Stages) { stage = 0; phase ^= 1; }
         }
+        if constexpr (kGather) {
+          __syncwarp();  // lane 0 has seen the stage free
+          if (!(p.debug & 2))
+            tma_gather4_2sm(smem_b + stage * S::kBBytes + lane * 512, &tmap_x, fb, kb * kGemmBK,
+                            idx0, idx1, idx2, idx3, pol_x);
+        }
+        if (++stage == k2Stages) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {

@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(256) permute_kernel(PermuteParams p) {
     }
     const int4* src = reinterpret_cast<const int4*>(p.x + static_cast<long>(t) * p.d);
     const bool any = dest[0] >= 0 || dest[1] >= 0;
-    if (any) {
+    if (any && p.x_perm) {
       int4* d0 = dest[0] >= 0 ? reinterpret_cast<int4*>(p.x_perm + static_cast<long>(dest[0]) * p.d) : nullptr;
       int4* d1 = dest[1] >= 0 ? reinterpret_cast<int4*>(p.x_perm + static_cast<long>(dest[1]) * p.d) : nullptr;
       for (int i0 = 0; i0 < vec; i0 += 32 * kRowUnroll) {
@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(256) permute_kernel(PermuteParams p) {
           }
         }
       }
-    } else if (p.y) {
+    } else if (!any && p.y) {
       int4* yr = reinterpret_cast<int4*>(p.y + static_cast<long>(t) * p.d);
       const int4 z = make_int4(0, 0, 0, 0);
       for (int i = lane; i < vec; i += 32) yr[i] = z;
@@ -139,9 +139,9 @@ int comoe_permute(const void* x, int T, int d, int top_k, const int* group_idx,
                   const int* group_base, int n_groups, int capacity, void* x_perm,
                   int* row_token, float* row_prob, int* token_pos, void* y_zero, void* stream) {
   using namespace comoe;
-  COMOE_REQUIRE(x && group_idx && gate_prob && local_rank && tile_offset && group_base && x_perm &&
+  COMOE_REQUIRE(x && group_idx && gate_prob && local_rank && tile_offset && group_base &&
                     row_token && row_prob && token_pos,
-                kBadArg, "permute: null pointer");
+                kBadArg, "permute: null pointer");  // x_perm may be NULL: index-only
   COMOE_REQUIRE(top_k == 1 || top_k == 2, kUnsupportedShape, "permute: top_k=%d", top_k);
   COMOE_REQUIRE(d % 8 == 0 && d > 0, kUnsupportedShape, "permute: d=%d must be a multiple of 8", d);
   COMOE_REQUIRE(T >= 0 && n_groups >= 1, kBadArg, "permute: bad sizes");

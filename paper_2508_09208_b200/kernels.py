@@ -151,7 +151,7 @@ class PermuteOutput:
 
 
 def permute(x, gate: GateOutput, scan: ScanOutput, capacity: int, rows: int,
-            y_zero=None, out: PermuteOutput = None) -> PermuteOutput:
+            y_zero=None, out: PermuteOutput = None, copy_rows: bool = True) -> PermuteOutput:
     _need(x, "x", torch.bfloat16, 2)
     T, d = x.shape
     k = gate.group_idx.shape[1]
@@ -166,8 +166,8 @@ def permute(x, gate: GateOutput, scan: ScanOutput, capacity: int, rows: int,
         _need(y_zero, "y_zero", torch.bfloat16, 2)
     _lib.call("comoe_permute", _ptr(x), T, d, k, _ptr(gate.group_idx), _ptr(gate.gate_prob),
               _ptr(gate.local_rank), _ptr(scan.tile_offset), _ptr(scan.group_base), G,
-              int(capacity), _ptr(out.x_perm), _ptr(out.row_token), _ptr(out.row_prob),
-              _ptr(out.token_pos), _ptr(y_zero), _stream())
+              int(capacity), _ptr(out.x_perm) if copy_rows else None, _ptr(out.row_token),
+              _ptr(out.row_prob), _ptr(out.token_pos), _ptr(y_zero), _stream())
     return out
 
 
@@ -213,7 +213,7 @@ def grouped_ffn(x_perm, pool, d_ff, act, group_rows, group_row_base, group_slot,
 
 
 def grouped_gemm(a, pool, b_offset, N, group_rows, group_row_base, group_slot, epi_mode, out,
-                 row_token=None, row_prob=None):
+                 row_token=None, row_prob=None, a_gather=None):
     _need(a, "a", torch.bfloat16, 2)
     _need(pool, "pool", torch.bfloat16, 2)
     _need(out, "out", torch.bfloat16, 2)
@@ -221,7 +221,7 @@ def grouped_gemm(a, pool, b_offset, N, group_rows, group_row_base, group_slot, e
     _lib.call("comoe_grouped_gemm", _ptr(a), rows, _ptr(pool), pool.shape[0], pool.shape[1],
               int(b_offset), int(N), K, _ptr(group_rows), _ptr(group_row_base),
               _ptr(group_slot), group_rows.numel(), int(epi_mode), _ptr(out), out.shape[1],
-              _ptr(row_token), _ptr(row_prob), _stream())
+              _ptr(row_token), _ptr(row_prob), _ptr(a_gather), _stream())
     return out
 
 

@@ -22,7 +22,16 @@ import torch
 from . import kernels
 from .pool import ExpertPool
 
+import os
+
 ACTS = {"relu": kernels.ACT_RELU, "swiglu": kernels.ACT_SWIGLU}
+
+
+def _gather_enabled(act: str) -> bool:
+    """GEMM1 gathers token rows with TMA (no permuted copy) on the 2-SM ReLU
+    kernel; SwiGLU (1-SM kernel) and COMOE_GEMM_1SM=1 keep the permute copy."""
+    return act == "relu" and os.environ.get("COMOE_GEMM_1SM", "0") != "1" and \
+        os.environ.get("COMOE_NO_GATHER", "0") != "1"
 
 
 class _NoTimer:
@@ -164,16 +173,17 @@ class MoELayer:
         with stage("route"):
             r = self.route(x, want_logits)
         k1 = self.top_k == 1
+        gather = _gather_enabled(self.act)
         with stage("permute"):
             kernels.permute(x, r.gate, r.scan, r.capacity, r.rows, y_zero=out if k1 else None,
-                            out=r.perm)
+                            out=r.perm, copy_rows=not gather)
         dst = out if k1 else ws["y_perm"]
         n1 = 2 * self.d_ff if self.act == "swiglu" else self.d_ff
         with stage("ffn1"):
-            kernels.grouped_gemm(r.perm.x_perm, self.pool.data, 0, n1, r.scan.group_kept,
-                                 r.scan.group_base, self.group_slot,
+            kernels.grouped_gemm(x if gather else r.perm.x_perm, self.pool.data, 0, n1,
+                                 r.scan.group_kept, r.scan.group_base, self.group_slot,
                                  kernels.EPI_SWIGLU if self.act == "swiglu" else kernels.EPI_RELU,
-                                 ws["h"])
+                                 ws["h"], a_gather=r.perm.row_token if gather else None)
         with stage("ffn2"):
             kernels.grouped_gemm(ws["h"], self.pool.data, n1 * self.d, self.d, r.scan.group_kept,
                                  r.scan.group_base, self.group_slot,
