@@ -28,10 +28,12 @@ ACTS = {"relu": kernels.ACT_RELU, "swiglu": kernels.ACT_SWIGLU}
 
 
 def _gather_enabled(act: str) -> bool:
-    """GEMM1 gathers token rows with TMA (no permuted copy) on the 2-SM ReLU
-    kernel; SwiGLU (1-SM kernel) and COMOE_GEMM_1SM=1 keep the permute copy."""
+    """Opt-in (COMOE_GATHER=1): GEMM1 gathers token rows with TMA gather4
+    instead of reading the permuted copy. Correct, but measured 3.3x slower
+    for GEMM1 at C2 (830 vs 255 us: 32 four-row gathers per k-block per CTA
+    saturate the TMA unit), so the permute copy (42 us) stays the default."""
     return act == "relu" and os.environ.get("COMOE_GEMM_1SM", "0") != "1" and \
-        os.environ.get("COMOE_NO_GATHER", "0") != "1"
+        os.environ.get("COMOE_GATHER", "0") == "1"
 
 
 class _NoTimer:
