@@ -70,6 +70,16 @@ int comoe_gate_topk(const void* x, int T, int d, const void* wg_split, int E, in
                     int* expert_idx, int* group_idx, float* gate_prob, int* local_rank,
                     int* tile_hist, void* stream);
 
+/* Replayed routing: the tables comoe_gate_topk produces after top-k, from
+ * given expert choices expert_idx[T,k] (a reference RoutingTrace,
+ * pkg/src/comoe/moe.py:146-162, or any external router) and optional
+ * probabilities probs[T,k] (NULL -> 1/k). Same slot remap, fold, tile
+ * ranks and histograms; G <= 1024.
+ */
+int comoe_route_from_indices(const int* expert_idx, const float* probs, int T, int E, int top_k,
+                             const int* slot_map, int n_groups, int* group_idx, float* gate_prob,
+                             int* local_rank, int* tile_hist, void* stream);
+
 /* ---------------------------------------------------------------- routing scan
  * Capacity in stream order (first choices in token order, then second
  * choices): tile_offset = exclusive scan of tile_hist per group,

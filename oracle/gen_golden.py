@@ -210,8 +210,32 @@ def policy_cases(off, n_cases=60):
     return cases
 
 
+def traces_and_predictor(moe, off):
+    out = []
+    for i, (E, K, skew, rho, n) in enumerate(((8, 1, 1.0, 0.9, 40), (16, 2, {"default": 0.5, 3: 2.0}, 0.5, 30),
+                                              (128, 1, 1.2, 1.0, 20))):
+        spec = moe.MoeModelSpec(total_layers=6, encoder_moe_layers=(1, 3), decoder_moe_layers=(5,),
+                                experts_per_layer=E, expert_size_bytes=1e6, top_k=K)
+        g = moe.RoutingGeneratorSpec(skew=skew, rho=rho, seed=10 + i, structure_seed=3 + i)
+        tr = moe.generate_routing(g, spec, n)
+        rec = dict(E=E, K=K, skew={str(k): v for k, v in skew.items()} if isinstance(skew, dict) else skew,
+                   rho=rho, seed=10 + i, structure_seed=3 + i, n=n,
+                   experts=[[list(tok.layer_experts[l]) for l in spec.moe_layer_indices] for tok in tr.tokens],
+                   emb_sum=float(sum(float(t.embedding.sum()) for t in tr.tokens)),
+                   ctx_sum=float(sum(float(t.context.sum()) for t in tr.tokens)))
+        if i == 0:
+            big = moe.generate_routing(g, spec, 300)
+            mlp, metrics = off.train_predictor(big, hidden_dim=8, lr=0.05, epochs=2, seed=5)
+            rec["predictor"] = dict(n=300, hidden=8, epochs=2, seed=5, w1=mlp.w1.tolist(),
+                                    b1=mlp.b1.tolist(), w2=mlp.w2.tolist(), b2=mlp.b2.tolist(),
+                                    metrics=metrics)
+        out.append(rec)
+    return out
+
+
 def main():
     moe, agg, off = _ref()
+    (OUT / "traces.json").write_text(json.dumps(traces_and_predictor(moe, off)))
     OUT.mkdir(parents=True, exist_ok=True)
     (OUT / "fusion_cases.json").write_text(json.dumps(fusion_cases(moe, agg)))
     (OUT / "merge_hand.json").write_text(json.dumps(merge_hand(moe, agg), indent=1))

@@ -28,6 +28,7 @@ _SIGNATURES = {
     "comoe_gate_prepare": [_p, _c_int, _c_int, _p, _p],
     "comoe_gate_topk": [_p, _c_int, _c_int, _p, _c_int, _c_int, _c_int, _p, _c_int, _p,
                         _p, _p, _p, _p, _p, _p],
+    "comoe_route_from_indices": [_p, _p, _c_int, _c_int, _c_int, _p, _c_int, _p, _p, _p, _p, _p],
     "comoe_route_scan": [_p, _c_int, _c_int, _c_int, _c_int, _p, _p, _p, _p, _p],
     "comoe_expert_histogram": [_p, _c_long, _c_int, _p, _p],
     "comoe_permute": [_p, _c_int, _c_int, _c_int, _p, _p, _p, _p, _p, _c_int, _c_int, _p,

@@ -391,9 +391,96 @@ __global__ void expert_hist_kernel(const int* __restrict__ idx, long n, int E,
     if (h[e]) atomicAdd(&counts[e], h[e]);
 }
 
+// Replayed routing (trace-driven runs): the same tile ranks / histograms as the
+// gate epilogue, from given expert choices instead of logits. One 128-thread
+// block per 128-token tile, thread = token.
+__global__ void __launch_bounds__(128) route_from_indices_kernel(
+    const int* __restrict__ expert_idx, const float* __restrict__ probs, int T, int E, int top_k,
+    const int* __restrict__ slot_map, int G, int ntiles, int* __restrict__ group_idx,
+    float* __restrict__ gate_prob, int* __restrict__ local_rank, int* __restrict__ tile_hist) {
+  __shared__ int cnt[kGateMaxK * 4 * 1024];
+  const int tile = blockIdx.x;
+  const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = tile * 128 + threadIdx.x;
+  const bool valid = t < T;
+  for (int i = threadIdx.x; i < top_k * 4 * G; i += 128) cnt[i] = 0;
+  __syncthreads();
+  int e0 = -1, e1 = -1;
+  float p0 = 0.f, p1 = 0.f;
+  if (valid) {
+    e0 = expert_idx[static_cast<long>(t) * top_k];
+    p0 = probs ? probs[static_cast<long>(t) * top_k] : 1.f / top_k;
+    if (top_k == 2) {
+      e1 = expert_idx[static_cast<long>(t) * top_k + 1];
+      p1 = probs ? probs[static_cast<long>(t) * top_k + 1] : 0.5f;
+    }
+  }
+  int g0 = (e0 >= 0 && e0 < E) ? (slot_map ? slot_map[e0] : e0) : -1;
+  int g1 = (e1 >= 0 && e1 < E) ? (slot_map ? slot_map[e1] : e1) : -1;
+  if (g1 >= 0 && g1 == g0) {
+    p0 += p1;
+    p1 = 0.f;
+    g1 = -1;
+  }
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  const unsigned m0 = __match_any_sync(0xffffffffu, g0);
+  const int wr0 = __popc(m0 & lt_mask);
+  if (g0 >= 0 && wr0 == 0) cnt[q * G + g0] = __popc(m0);
+  int wr1 = 0;
+  if (top_k == 2) {
+    const unsigned m1 = __match_any_sync(0xffffffffu, g1);
+    wr1 = __popc(m1 & lt_mask);
+    if (g1 >= 0 && wr1 == 0) cnt[(4 + q) * G + g1] = __popc(m1);
+  }
+  __syncthreads();
+  if (valid) {
+    const long o = static_cast<long>(t) * top_k;
+    int r0 = -1, r1 = -1;
+    if (g0 >= 0) {
+      r0 = wr0;
+      for (int qq = 0; qq < q; ++qq) r0 += cnt[qq * G + g0];
+    }
+    group_idx[o] = g0;
+    gate_prob[o] = g0 >= 0 ? p0 : 0.f;
+    local_rank[o] = r0;
+    if (top_k == 2) {
+      if (g1 >= 0) {
+        r1 = wr1;
+        for (int qq = 0; qq < q; ++qq) r1 += cnt[(4 + qq) * G + g1];
+      }
+      group_idx[o + 1] = g1;
+      gate_prob[o + 1] = g1 >= 0 ? p1 : 0.f;
+      local_rank[o + 1] = r1;
+    }
+  }
+  for (int j = 0; j < top_k; ++j)
+    for (int g = threadIdx.x; g < G; g += 128) {
+      int h = 0;
+      for (int qq = 0; qq < 4; ++qq) h += cnt[(j * 4 + qq) * G + g];
+      tile_hist[(static_cast<long>(j) * ntiles + tile) * G + g] = h;
+    }
+}
+
 }  // namespace comoe
 
 extern "C" {
+
+int comoe_route_from_indices(const int* expert_idx, const float* probs, int T, int E, int top_k,
+                             const int* slot_map, int n_groups, int* group_idx, float* gate_prob,
+                             int* local_rank, int* tile_hist, void* stream) {
+  using namespace comoe;
+  COMOE_REQUIRE(expert_idx && group_idx && gate_prob && local_rank && tile_hist, kBadArg,
+                "route_from_indices: null pointer");
+  COMOE_REQUIRE(top_k == 1 || top_k == 2, kUnsupportedShape, "route_from_indices: top_k=%d", top_k);
+  COMOE_REQUIRE(n_groups >= 1 && n_groups <= 1024 && E >= 1, kBadArg,
+                "route_from_indices: n_groups=%d", n_groups);
+  if (T <= 0) return kOk;
+  const int nt = (T + 127) / 128;
+  route_from_indices_kernel<<<nt, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      expert_idx, probs, T, E, top_k, slot_map, n_groups, nt, group_idx, gate_prob, local_rank,
+      tile_hist);
+  return check_launch("route_from_indices_kernel");
+}
 
 int comoe_gate_padded_experts(int E) {
   if (E < 1 || E > comoe::kGateMaxE) return -1;

@@ -111,6 +111,31 @@ def gate_topk(x, wg_split, E, top_k, norm_topk, slot_map=None, n_groups=None,
     return out
 
 
+def route_from_indices(expert_idx, E, probs=None, slot_map=None, n_groups=None,
+                       out: GateOutput = None) -> GateOutput:
+    """Routing tables from given expert choices (trace replay)."""
+    _need(expert_idx, "expert_idx", torch.int32, 2)
+    T, k = expert_idx.shape
+    G = E if n_groups is None else int(n_groups)
+    if probs is not None:
+        _need(probs, "probs", torch.float32, 2)
+    if slot_map is not None:
+        _need(slot_map, "slot_map", torch.int32, 1)
+    nt = gate_num_tiles(T)
+    dev = expert_idx.device
+    if out is None:
+        out = GateOutput(expert_idx, torch.empty((T, k), dtype=torch.int32, device=dev),
+                         torch.empty((T, k), dtype=torch.float32, device=dev),
+                         torch.empty((T, k), dtype=torch.int32, device=dev),
+                         torch.empty((k, nt, G), dtype=torch.int32, device=dev))
+    else:
+        out.expert_idx.copy_(expert_idx)
+    _lib.call("comoe_route_from_indices", _ptr(expert_idx), _ptr(probs), T, E, k,
+              _ptr(slot_map), G, _ptr(out.group_idx), _ptr(out.gate_prob), _ptr(out.local_rank),
+              _ptr(out.tile_hist), _stream())
+    return out
+
+
 @dataclass
 class ScanOutput:
     tile_offset: torch.Tensor  # [k, ntiles, G]

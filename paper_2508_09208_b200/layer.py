@@ -145,11 +145,22 @@ class MoELayer:
         return ws
 
     # ------------------------------------------------------------ forward
-    def route(self, x: torch.Tensor, want_logits: bool = False) -> LayerRouting:
+    def route(self, x: torch.Tensor, want_logits: bool = False, routing=None) -> LayerRouting:
+        """Gate + capacity scan. `routing` = (expert_idx [T,k] int32, probs
+        [T,k] float32 or None) replays given choices (e.g. a reference
+        RoutingTrace) instead of running the router."""
         kernels._need(x, "x", torch.bfloat16, 2)
         T = x.shape[0]
         ws = self._workspace(T)
         gate = ws["gate"]
+        if routing is not None:
+            idx, probs = routing
+            if tuple(idx.shape) != (T, self.top_k):
+                raise ValueError(f"routing must be [T, {self.top_k}]")
+            kernels.route_from_indices(idx.to(torch.int32).contiguous(), self.E, probs=probs,
+                                       slot_map=self.slot_map, n_groups=self.G, out=gate)
+            kernels.route_scan(gate.tile_hist, ws["C"], out=ws["scan"])
+            return LayerRouting(gate, ws["scan"], ws["perm"], ws["C"], ws["rows"])
         if want_logits:
             gate = kernels.GateOutput(gate.expert_idx, gate.group_idx, gate.gate_prob,
                                       gate.local_rank, gate.tile_hist,
@@ -160,7 +171,7 @@ class MoELayer:
         return LayerRouting(gate, ws["scan"], ws["perm"], ws["C"], ws["rows"])
 
     def forward(self, x: torch.Tensor, out: torch.Tensor = None,
-                want_logits: bool = False, timer=None) -> torch.Tensor:
+                want_logits: bool = False, timer=None, routing=None) -> torch.Tensor:
         """`timer`: optional callable(name) -> context manager recording
         CUDA events around each stage on the current stream (bench.py)."""
         if x.shape[1] != self.d:
@@ -173,7 +184,7 @@ class MoELayer:
         ws = self._workspace(T)
         stage = timer if timer is not None else _no_timer
         with stage("route"):
-            r = self.route(x, want_logits)
+            r = self.route(x, want_logits, routing=routing)
         k1 = self.top_k == 1
         gather = _gather_enabled(self.act)
         with stage("permute"):

@@ -16,6 +16,8 @@ import numpy as np
 import torch
 
 from . import kernels
+from .traces import (RoutingGeneratorSpec, RoutingTrace, TokenRecord,  # noqa: F401
+                     generate_routing, trace_from_jsonl, trace_to_jsonl)
 
 
 @dataclass

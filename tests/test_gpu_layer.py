@@ -183,3 +183,46 @@ def test_full_size_properties_sb128():
         ref[i] = prob[t, 0] * O.expert_ffn(xs[i:i + 1], w_in, w_out, "relu")[0]
     assert O.normwise_error(y[torch.as_tensor(toks).cuda()].float().cpu().numpy(), ref) < NORMWISE_TOL
     assert torch.all(y[torch.as_tensor(np.nonzero(pos < 0)[0]).cuda()] == 0)
+
+
+def test_replayed_trace_routing_matches_oracle():
+    """A reference-style RoutingTrace replayed through the device layer
+    (comoe_route_from_indices): tables and outputs equal the oracle given the
+    same expert choices (top-2, with a merge that folds pairs)."""
+    from paper_2508_09208_b200 import ExpertPool, MoELayer, kernels
+    from paper_2508_09208_b200.moe import MoeModelSpec, RoutingGeneratorSpec, generate_routing
+    T, d, d_ff, E = 700, 256, 512, 8
+    spec = MoeModelSpec(total_layers=2, encoder_moe_layers=(1,), decoder_moe_layers=(),
+                        experts_per_layer=E, expert_size_bytes=1.0, top_k=2)
+    tr = generate_routing(RoutingGeneratorSpec(skew=1.0, seed=3), spec, T)
+    idx = tr.expert_indices(1)
+    x, wg, w = _layer_inputs(T, d, d_ff, E, "relu", seed=5)
+    pool = ExpertPool(E, w.shape[1])
+    pool.data[:, : w.shape[1]].copy_(w.cuda())
+    layer = MoELayer(wg, pool, d_ff, act="relu", top_k=2, capacity_factor=1.0)
+    slot_map = [0, 1, 2, 3, 0, 1, 2, 3]
+    layer.set_variant(slot_map, [0, 1, 2, 3])
+    probs = np.full((T, 2), 0.5, np.float32)
+    y = layer.forward(x, routing=(torch.as_tensor(idx).cuda(), torch.as_tensor(probs).cuda()))
+    torch.cuda.synchronize()
+    g = layer.last.gate
+    group = np.asarray(slot_map)[idx]
+    pr = probs.astype(np.float64).copy()
+    same = group[:, 1] == group[:, 0]
+    pr[same, 0] += pr[same, 1]
+    pr[same, 1] = 0
+    group[same, 1] = -1
+    C = O.capacity(T, 4, 2, 1.0)
+    disp = O.dispatch(group, 4, C)
+    np.testing.assert_array_equal(g.group_idx.cpu().numpy(), group)
+    np.testing.assert_array_equal(g.local_rank.cpu().numpy(), disp["local_rank"])
+    np.testing.assert_array_equal(layer.last.perm.token_pos.cpu().numpy(), disp["pos"])
+    xs = _np(x)
+    ref = np.zeros((T, d))
+    for t in range(T):
+        for j in range(2):
+            p_ = disp["pos"][t, j]
+            if p_ >= 0:
+                w_in, w_out = O.split_expert(_np(w[group[t, j]]), d, d_ff, "relu")
+                ref[t] += pr[t, j] * O.expert_ffn(xs[t:t + 1], w_in, w_out, "relu")[0]
+    assert O.normwise_error(_np(y), ref) < NORMWISE_TOL
