@@ -260,7 +260,10 @@ class CachedMoELayer:
         self._tables = torch.zeros((self.E, 2, self.E), dtype=torch.int32).pin_memory()
         self._tables_dev = torch.zeros((self.E, 2, self.E), dtype=torch.int32, device=wg.device)
 
-    def forward(self, x, out=None):
+    def forward(self, x, out=None, after_route=None):
+        """`after_route(routing)` runs after the demand set is known and before
+        the GEMMs are enqueued: the stack issues the next layer's prefetch
+        there so its copies overlap this layer's expert GEMMs."""
         L = self.layer
         T = x.shape[0]
         if out is None:
@@ -272,6 +275,8 @@ class CachedMoELayer:
         kernels.permute(x, r.gate, r.scan, r.capacity, r.rows, y_zero=out if k1 else None,
                         out=r.perm)
         kept = r.scan.group_kept.cpu().numpy()  # the demand set (the layer's one host sync)
+        if after_route is not None:
+            after_route(r)
         c = self.cache
         c.tick += 1
         order = [int(g) for g in np.argsort(-kept, kind="stable") if kept[g] > 0]

@@ -1,0 +1,62 @@
+"""Multi-layer MoE stack on HBM-budgeted expert caches with predictive
+prefetch — the per-token policy loop of the reference simulator
+(simulator.py:684-724: serve demand, predict the next MoE layer, prefetch,
+evict) turned into a batched device pipeline.
+
+For each MoE layer l of the stack:
+  1. route layer l (gate + scan) and serve its demand from cache_l (hits,
+     substitutions, demand fetches — CachedMoELayer);
+  2. if l is an encoder layer with a successor (simulator.py:709-712), run
+     the K8 predictor on layer l's routing for every token, reduce to the
+     expected per-expert demand of layer l+1 (mean probability over tokens,
+     the batched stand-in for the per-token probabilities the reference
+     passes to decide_prefetch), and prefetch into cache_{l+1} with the
+     resource-aware threshold. The copies run on cache_{l+1}'s copy stream
+     and overlap layer l's grouped GEMMs;
+  3. decoder layers can be pinned (pin_decoder, simulator.py:407-413).
+Dense (non-MoE) sublayers are outside this hot path; hidden states pass
+between MoE layers unchanged (x_{l+1} = y_l + x_l residual).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from .offload import OffloadPolicy, prefetch_threshold
+
+
+@dataclass
+class StackLayer:
+    index: int
+    layer: object            # CachedMoELayer
+    encoder: bool = True
+
+
+class CachedMoEStack:
+    def __init__(self, layers: list, predictor=None, policy: OffloadPolicy = None,
+                 s_b: float = 1.0, mem_avail: float = 1.0, mem_total: float = 1.0):
+        self.layers = layers
+        self.predictor = predictor
+        self.policy = policy or OffloadPolicy()
+        self.theta = prefetch_threshold(self.policy, s_b, mem_avail, mem_total)
+        self.prefetch_log = []
+
+    def forward(self, x, emb=None, ctx=None):
+        """x [T, d] bf16; emb/ctx [T, *] float64 device tensors for the
+        predictor (token embedding / context, as TokenRecord carries)."""
+        h = x
+        for i, sl in enumerate(self.layers):
+            nxt = self.layers[i + 1] if i + 1 < len(self.layers) else None
+            hook = None
+            if nxt is not None and sl.encoder and self.predictor is not None:
+                def hook(r, sl=sl, nxt=nxt):
+                    probs = self.predictor.predict_slots(r.gate.expert_idx, emb, ctx)
+                    demand = probs.mean(dim=0).cpu().numpy()
+                    chosen = nxt.layer.cache.prefetch(demand, self.theta)
+                    self.prefetch_log.append((sl.index, nxt.index, chosen))
+            y = sl.layer.forward(h, after_route=hook)
+            h = (y.float() + h.float()).to(torch.bfloat16)
+        return h

@@ -62,3 +62,42 @@ def test_cached_layer_skewed_small_batches_hit_and_prefetch():
     assert chosen and all(cache.state.resident(e) for e in chosen)
     assert cache.stats.prefetch_issued == len(chosen)
     cache.check()
+
+
+def test_cached_stack_predictive_prefetch():
+    """Two-layer stack: the K8 predictor on layer 1's routing drives
+    prefetches into layer 2's cache; outputs equal the all-resident stack."""
+    from paper_2508_09208_b200 import ExpertPool, MoELayer, kernels
+    from paper_2508_09208_b200.cache import CachedMoELayer, ExpertCache
+    from paper_2508_09208_b200.offload import OffloadPolicy, PredictorMLP
+    from paper_2508_09208_b200.stack import CachedMoEStack, StackLayer
+    T, d, d_ff, E = 256, 256, 512, 16
+    g = torch.Generator().manual_seed(9)
+    x = torch.randn(T, d, generator=g).to(torch.bfloat16).cuda()
+    numel = kernels.expert_numel(d, d_ff, kernels.ACT_RELU)
+    layers, refs = [], []
+    for l in range(2):
+        wg = (torch.randn(d, E, generator=g) / math.sqrt(d)).cuda()
+        w = (torch.randn(E, numel, generator=g) * 0.02).to(torch.bfloat16)
+        pool = ExpertPool(E, numel)
+        pool.data[:, :numel].copy_(w.cuda())
+        refs.append(MoELayer(wg, pool, d_ff, capacity_factor=2.0))
+        cache = ExpertCache(w.contiguous().pin_memory(), layer=l + 1, n_slots=6, workspace_slots=1)
+        layers.append(StackLayer(l + 1, CachedMoELayer(wg, cache, d_ff, capacity_factor=2.0)))
+    rng = np.random.default_rng(0)
+    mlp = PredictorMLP(w1=rng.normal(scale=0.5, size=(32, E + 4 + 2)), b1=np.zeros(32),
+                       w2=rng.normal(scale=2.0, size=(E, 32)), b2=np.zeros(E),
+                       experts_per_layer=E, embed_dim=4, context_dim=2)
+    emb = torch.randn(T, 4, dtype=torch.float64, generator=g).cuda()
+    ctx = torch.randn(T, 2, dtype=torch.float64, generator=g).cuda()
+    stack = CachedMoEStack(layers, predictor=mlp,
+                           policy=OffloadPolicy(threshold_mode="constant", theta_base=0.05))
+    y = stack.forward(x, emb, ctx)
+    h = x
+    for ref in refs:
+        h = (ref.forward(h).float() + h.float()).to(torch.bfloat16)
+    torch.cuda.synchronize()
+    assert torch.equal(y, h)
+    assert len(stack.prefetch_log) == 1
+    for sl in layers:
+        sl.layer.cache.check()

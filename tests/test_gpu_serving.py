@@ -65,3 +65,4 @@ def test_expert_parallel_world1_matches_oracle():
                                      dtype=np.float64)
     assert (info["pos"] < 0).sum() > 0
     assert O.normwise_error(y.float().cpu().numpy(), ref) < 1e-2
+    dist.destroy_process_group()
