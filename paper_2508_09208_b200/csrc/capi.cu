@@ -59,6 +59,27 @@ int make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_
   return kOk;
 }
 
+int make_tmap_bf16_2d_box(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                          uint64_t row_stride_elems, uint32_t box_cols, uint32_t box_rows,
+                          int swizzle_bytes) {
+  std::call_once(g_encode_once, load_encode);
+  COMOE_REQUIRE(g_encode != nullptr, kNoDriver, "cuTensorMapEncodeTiled unavailable (no driver)");
+  COMOE_REQUIRE((reinterpret_cast<uintptr_t>(base) & 15) == 0 && row_stride_elems % 8 == 0,
+                kBadArg, "tensor base/stride must be 16-byte aligned");
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {row_stride_elems * 2};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  const CUtensorMapSwizzle sw = swizzle_bytes == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                      : CU_TENSOR_MAP_SWIZZLE_NONE;
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  COMOE_REQUIRE(r == CUDA_SUCCESS, kCudaError, "cuTensorMapEncodeTiled(box) failed (%d)", (int)r);
+  return kOk;
+}
+
 int make_tmap_bf16_3d(CUtensorMap* map, const void* base, uint64_t slots, uint64_t rows,
                       uint64_t cols, uint64_t slot_stride, uint32_t box_rows) {
   std::call_once(g_encode_once, load_encode);

@@ -42,6 +42,10 @@ int check_launch(const char* what);
 // 64 cols] with 128-byte swizzle (64 bf16 = 128 B per box row).
 int make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t rows,
                       uint64_t cols, uint32_t box_rows);
+// 2-D bf16 tensor map with an explicit box and swizzle (0 none, 64, 128 bytes)
+int make_tmap_bf16_2d_box(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                          uint64_t row_stride_elems, uint32_t box_cols, uint32_t box_rows,
+                          int swizzle_bytes);
 // 3-D bf16 tensor map over `slots` row-major [rows, cols] matrices whose bases
 // are slot_stride elements apart (the expert slot pool); box = [1, box_rows, 64].
 int make_tmap_bf16_3d(CUtensorMap* map, const void* base, uint64_t slots, uint64_t rows,
@@ -121,6 +125,23 @@ __device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* m
       " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z), "l"(policy)
       : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int32_t x,
+                                             int32_t y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(x), "r"(y)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 __device__ __forceinline__ uint64_t l2_policy_evict_first() {
   uint64_t p;

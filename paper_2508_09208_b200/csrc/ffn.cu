@@ -29,7 +29,8 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const Group
 
 template <int kMode, int kStages, int kEpiWarps>
 static int launch_gemm_2sm_cfg(const CUtensorMap& tw, const CUtensorMap& tx,
-                               const GroupedGemmParams& p, cudaStream_t stream) {
+                               const CUtensorMap& to, const GroupedGemmParams& p,
+                               cudaStream_t stream) {
   using C = Gemm2Cfg<kStages, kEpiWarps>;
   if (p.gather_rows) {
     if constexpr (kMode == kEpiRelu) {
@@ -42,7 +43,7 @@ static int launch_gemm_2sm_cfg(const CUtensorMap& tw, const CUtensorMap& tx,
       int dev = 0, sms = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      kg<<<sms & ~1, C::kThreads, C::kTotal, stream>>>(tw, tx, p);
+      kg<<<sms & ~1, C::kThreads, C::kTotal, stream>>>(tw, tx, to, p);
       return check_launch("grouped_gemm_2sm_kernel(gather)");
     }
     set_error("grouped_gemm: row gather is only supported with the ReLU epilogue");
@@ -57,12 +58,12 @@ static int launch_gemm_2sm_cfg(const CUtensorMap& tw, const CUtensorMap& tx,
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  kern<<<sms & ~1, C::kThreads, C::kTotal, stream>>>(tw, tx, p);
+  kern<<<sms & ~1, C::kThreads, C::kTotal, stream>>>(tw, tx, to, p);
   return check_launch("grouped_gemm_2sm_kernel");
 }
 
-// pipeline config (COMOE_GEMM2_CFG=0..3 for A/B runs): 0 = 6 stages x 8 epilogue
-// warps, 1 = 4 x 8, 2 = 6 x 4, 3 = 5 x 8
+// pipeline config (COMOE_GEMM2_CFG=0..2 for A/B runs): 0 = 5 stages x 8 epilogue
+// warps, 1 = 4 x 8, 2 = 6 x 4
 static int gemm2_cfg() {
   static const int c = [] {
     const char* e = std::getenv("COMOE_GEMM2_CFG");
@@ -72,13 +73,12 @@ static int gemm2_cfg() {
 }
 
 template <int kMode>
-static int launch_gemm_2sm(const CUtensorMap& tw, const CUtensorMap& tx,
+static int launch_gemm_2sm(const CUtensorMap& tw, const CUtensorMap& tx, const CUtensorMap& to,
                            const GroupedGemmParams& p, cudaStream_t stream) {
   switch (gemm2_cfg()) {
-    case 1: return launch_gemm_2sm_cfg<kMode, 4, 8>(tw, tx, p, stream);
-    case 2: return launch_gemm_2sm_cfg<kMode, 6, 4>(tw, tx, p, stream);
-    case 3: return launch_gemm_2sm_cfg<kMode, 5, 8>(tw, tx, p, stream);
-    default: return launch_gemm_2sm_cfg<kMode, 6, 8>(tw, tx, p, stream);
+    case 1: return launch_gemm_2sm_cfg<kMode, 4, 8>(tw, tx, to, p, stream);
+    case 2: return launch_gemm_2sm_cfg<kMode, 6, 4>(tw, tx, to, p, stream);
+    default: return launch_gemm_2sm_cfg<kMode, 5, 8>(tw, tx, to, p, stream);
   }
 }
 
@@ -132,10 +132,16 @@ static int grouped_gemm_impl(const void* a, long a_rows, const void* pool, int n
     if (rc) return rc;
     rc = make_tmap_bf16_2d(&ta, a, static_cast<uint64_t>(a_rows), K, a_gather ? 1 : 128);
     if (rc) return rc;
+    // output map for the bulk-store epilogue: [a_rows, N] bf16 at ld ldo, box
+    // 32 features x 32 tokens, 64-byte swizzle (unused by the scatter mode)
+    CUtensorMap to;
+    rc = make_tmap_bf16_2d_box(&to, out, static_cast<uint64_t>(a_rows), static_cast<uint64_t>(N),
+                               static_cast<uint64_t>(ldo), 32, 32, 64);
+    if (rc) return rc;
     switch (epi_mode) {
-      case kEpiRelu: return launch_gemm_2sm<kEpiRelu>(tb, ta, p, stream);
-      case kEpiScaleScatter: return launch_gemm_2sm<kEpiScaleScatter>(tb, ta, p, stream);
-      case kEpiStore: return launch_gemm_2sm<kEpiStore>(tb, ta, p, stream);
+      case kEpiRelu: return launch_gemm_2sm<kEpiRelu>(tb, ta, to, p, stream);
+      case kEpiScaleScatter: return launch_gemm_2sm<kEpiScaleScatter>(tb, ta, to, p, stream);
+      case kEpiStore: return launch_gemm_2sm<kEpiStore>(tb, ta, to, p, stream);
       default: break;
     }
     set_error("grouped_gemm: unknown epilogue mode %d", epi_mode);

@@ -34,7 +34,7 @@ struct Gemm2Cfg {
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTileBytes = kStages * kStageBytes;
   static constexpr int kXposeBytes = 0;                          // (register transpose)
-  static constexpr int kStgBytes = kEpiWarps * 32 * 64;        // per-warp 32 tokens x 32 feats
+  static constexpr int kStgBytes = kEpiWarps * 2 * 32 * 64;    // per-warp 2 x (32 tok x 32 feat)
   static constexpr int kCtrlBytes = (2 * kStages + 4) * 8 + 16 + (kMaxGroups2 + 1) * 4;
   static constexpr int kTotal = 1024 + kTileBytes + kXposeBytes + kStgBytes + kCtrlBytes;
   static_assert(kTotal <= 227 * 1024, "shared memory");
@@ -167,7 +167,8 @@ __device__ __forceinline__ Tile2 decode_tile2(const int* prefix, const GroupedGe
 template <int kMode, int k2Stages, int k2EpiWarps, bool kGather = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k2EpiWarps>::kThreads, 1)
     grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmap_w,
-                            const __grid_constant__ CUtensorMap tmap_x, GroupedGemmParams p) {
+                            const __grid_constant__ CUtensorMap tmap_x,
+                            const __grid_constant__ CUtensorMap tmap_out, GroupedGemmParams p) {
   static_assert(kMode != kEpiSwiGLU, "SwiGLU uses the 1-SM kernel");
   using S = Gemm2Cfg<k2Stages, k2EpiWarps>;
   extern __shared__ uint8_t smem_raw[];
@@ -306,7 +307,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k
     const int ew = warp - 4;
     const int q = warp & 3, sub = ew >> 2;
     constexpr int kSubs = k2EpiWarps / 4;
-    const uint32_t sg = smem_u32(stg) + ew * (32 * 64);
+    const uint32_t sg0 = smem_u32(stg) + ew * (2 * 32 * 64);
+    constexpr bool kTmaStore = kMode != kEpiScaleScatter;  // contiguous rows: TMA bulk store
+    int nbuf = 0;
     int it = 0;
     for (int tile = cluster; tile < total_tiles; tile += n_clusters, ++it) {
       const Tile2 t = decode_tile2(prefix, p, f_tiles, tile);
@@ -340,38 +343,59 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k
           for (int j = 0; j < 32; ++j)
             v[j] = __float_as_uint(__uint_as_float(v[j]) * __shfl_sync(0xffffffffu, my_p, j));
         }
-        // register transpose of feature pairs: lane 2p keeps tokens 0..15, lane 2p+1
-        // tokens 16..31; one shfl_xor per token swaps the partner feature in
-        const bool odd = lane & 1;
-        const uint32_t prow = static_cast<uint32_t>(lane >> 1);  // feature pair index
+        // register transpose of feature pairs: lanes (2p, 2p+1) hold features
+        // (2p, 2p+1); for each token pair (2j, 2j+1) the even lane keeps token
+        // 2j and the odd lane token 2j+1, one shfl_xor swapping the partner
+        // feature in. Staging = bf16 [32 tokens][32 features], 64-B rows in
+        // the TMA 64-byte swizzle (16-B chunk c at c ^ ((row/2)%4)): the
+        // even/odd lanes land in opposite bank halves -> conflict-free STS.
+        const int odd = lane & 1;
+        const uint32_t pw = static_cast<uint32_t>(lane >> 1);  // feature-pair word 0..15
+        const uint32_t sg = sg0 + nbuf * (32 * 64);
+        if constexpr (kTmaStore) {
+          if (lane == 0) bulk_wait_read<1>();  // this buffer's previous store has read smem
+          __syncwarp();
+        }
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          const float send = __uint_as_float(odd ? v[j] : v[16 + j]);
+          const float send = __uint_as_float(odd ? v[2 * j] : v[2 * j + 1]);
           const float recv = __shfl_xor_sync(0xffffffffu, send, 1);
-          const float lo = odd ? recv : __uint_as_float(v[j]);        // feature 2p
-          const float hi = odd ? __uint_as_float(v[16 + j]) : recv;   // feature 2p+1
-          const int tok_r = odd ? 16 + j : j;                          // staging row
-          // bf16 [32 tokens][32 features] rows of 64 B; word p ^ 8 in the upper 16 rows
-          // keeps the even/odd halves of the warp on different banks
-          const uint32_t word = prow ^ ((tok_r >> 4) << 3);
-          asm volatile("st.shared.b32 [%0], %1;" ::"r"(sg + tok_r * 64 + word * 4),
-                       "r"(pack_bf16x2(lo, hi))
-                       : "memory");
+          const float lo = odd ? recv : __uint_as_float(v[2 * j]);          // feature 2p
+          const float hi = odd ? __uint_as_float(v[2 * j + 1]) : recv;      // feature 2p+1
+          const uint32_t row = 2 * j + odd;
+          const uint32_t addr = sg + row * 64 + (((pw >> 2) ^ ((row >> 1) & 3)) << 4) + ((pw & 3) << 2);
+          asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(pack_bf16x2(lo, hi)) : "memory");
         }
         __syncwarp();
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int r = 8 * i + (lane >> 2), j = lane & 3;
-          const uint4 x = lds128(sg + r * 64 + ((j ^ ((r >> 4) << 1)) << 4));
-          const int tk = c + r;
-          if (tk < t.ntok) {
-            long dst;
-            if constexpr (kMode == kEpiScaleScatter) dst = __ldg(p.row_token + row_base + tk);
-            else dst = row_base + tk;
-            st_global_v4(p.out + dst * p.ldo + col0 + j * 8, x.x, x.y, x.z, x.w);
+        bool stored = false;
+        if constexpr (kTmaStore) {
+          if (c + 32 <= t.ntok) {  // whole chunk valid: one bulk tensor store
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmap_out, stg + (sg - smem_u32(stg)), static_cast<int>(col0),
+                           static_cast<int>(row_base + c));
+              bulk_commit();
+            }
+            nbuf ^= 1;
+            stored = true;
           }
         }
-        __syncwarp();
+        if (!stored) {  // scatter rows or a partial chunk: 16-B stores, 4 lanes per row
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int r = 8 * i + (lane >> 2), j = lane & 3;
+            const uint4 x = lds128(sg + r * 64 + ((j ^ ((r >> 1) & 3)) << 4));
+            const int tk = c + r;
+            if (tk < t.ntok) {
+              long dst;
+              if constexpr (kMode == kEpiScaleScatter) dst = __ldg(p.row_token + row_base + tk);
+              else dst = row_base + tk;
+              st_global_v4(p.out + dst * p.ldo + col0 + j * 8, x.x, x.y, x.z, x.w);
+            }
+          }
+          __syncwarp();
+        }
       }
       if (!released) {  // no chunk for this warp in a narrow tile
         tc_fence_before();
@@ -381,6 +405,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k
     }
   }
 
+  if (warp >= 4 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   tc_fence_before();
   cluster_sync_all();
   if (warp == 2) {
