@@ -19,6 +19,11 @@ namespace comoe {
 
 constexpr int kGateMaxE = 128;
 constexpr int kGateMaxK = 2;
+// w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-7 epilogue group 0 (accumulator 0,
+// even tiles of this CTA), w8-11 epilogue group 1 (accumulator 1, odd tiles):
+// two softmax/top-k/rank epilogues in flight per SM so the tensor core is not
+// paced by one (profiles: the MMA warp waited on tmem_empty with one group).
+constexpr int kGateThreads = 384;
 
 // ------------------------------------------------------------ weight split
 __global__ void gate_split_kernel(const float* __restrict__ wg, int d, int E, int EP,
@@ -56,12 +61,12 @@ struct GateSmem {
   static constexpr int kBBytes = 3 * EP * kGemmBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTileBytes = kStages * kStageBytes;
-  static constexpr int kCtrlBytes = (2 * kStages + 4) * 8 + 16 + kGateMaxK * 4 * kGateMaxE * 4 + kGateMaxE * 4;
+  static constexpr int kCtrlBytes = (2 * kStages + 4) * 8 + 16 + 2 * kGateMaxK * 4 * kGateMaxE * 4 + kGateMaxE * 4;
   static constexpr int kTotal = 1024 + kTileBytes + kCtrlBytes;
 };
 
 template <int EP, int kStages>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+__global__ void __launch_bounds__(kGateThreads, 1)
     gate_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 const __grid_constant__ CUtensorMap tmap_w, GateParams p) {
   using S = GateSmem<EP, kStages>;
@@ -78,8 +83,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* tfull_bar = empty_bar + kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
-  int* cnt = reinterpret_cast<int*>(tmem_slot + 4);       // [kMaxK][4][kGateMaxE]
-  int* smap = cnt + kGateMaxK * 4 * kGateMaxE;             // [kGateMaxE]
+  int* cnt_all = reinterpret_cast<int*>(tmem_slot + 4);   // [2 groups][kMaxK][4][kGateMaxE]
+  int* smap = cnt_all + 2 * kGateMaxK * 4 * kGateMaxE;     // [kGateMaxE]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -155,9 +160,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else if (warp >= 4) {
     const int q = warp & 3;
+    const int eg = (warp - 4) >> 2;                 // epilogue group = accumulator
+    const int et = threadIdx.x - 128 - 128 * eg;    // 0..127 inside the group
+    int* cnt = cnt_all + eg * kGateMaxK * 4 * kGateMaxE;
     const uint32_t lt_mask = (1u << lane) - 1u;
-    int it = 0;
-    for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++it) {
+    int it = eg;
+    for (int tile = blockIdx.x + eg * gridDim.x; tile < p.ntiles; tile += 2 * gridDim.x, it += 2) {
       const int acc = it & 1;
       const int t = tile * kGemmBM + q * 32 + lane;
       const bool valid = t < p.T;
@@ -237,9 +245,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
 
       // token-order ranks inside the tile: warp match + per-warp counts
-      named_bar_sync(1, 128);
-      for (int i = threadIdx.x - 128; i < p.top_k * 4 * kGateMaxE; i += 128) cnt[i] = 0;
-      named_bar_sync(1, 128);
+      named_bar_sync(1 + eg, 128);
+      for (int i = et; i < p.top_k * 4 * kGateMaxE; i += 128) cnt[i] = 0;
+      named_bar_sync(1 + eg, 128);
       int wr0, wr1 = 0;
       {
         const unsigned m0 = __match_any_sync(0xffffffffu, gr0);
@@ -251,7 +259,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if (gr1 >= 0 && wr1 == 0) cnt[(4 + q) * kGateMaxE + gr1] = __popc(m1);
         }
       }
-      named_bar_sync(1, 128);
+      named_bar_sync(1 + eg, 128);
       if (valid) {
         int rank0 = -1, rank1 = -1;
         if (gr0 >= 0) {
@@ -275,7 +283,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       }
       for (int j = 0; j < p.top_k; ++j)
-        for (int g = threadIdx.x - 128; g < p.G; g += 128) {
+        for (int g = et; g < p.G; g += 128) {
           int h = 0;
           if (g < kGateMaxE)
             for (int qq = 0; qq < 4; ++qq) h += cnt[(j * 4 + qq) * kGateMaxE + g];
@@ -307,7 +315,7 @@ static int launch_gate(const CUtensorMap& tx, const CUtensorMap& tw, const GateP
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = p.ntiles < sms ? p.ntiles : sms;
-  kern<<<grid, kGemmThreads, S::kTotal, stream>>>(tx, tw, p);
+  kern<<<grid, kGateThreads, S::kTotal, stream>>>(tx, tw, p);
   return check_launch("gate_kernel");
 }
 
