@@ -26,19 +26,33 @@ struct PermuteParams {
   __nv_bfloat16* y;    // optional: zero rows of fully-dropped tokens (top-1 fused combine)
 };
 
-constexpr int kRowUnroll = 4;
+constexpr int kRowUnroll = 3;  // d = 768: one slice covers the row
 
 constexpr int kTokPerWarp = 4;
 
-// One warp per kTokPerWarp consecutive tokens: ranks -> destinations, then the
-// rows are copied with every lane keeping kTokPerWarp*ceil(d/256) 16-byte
-// loads in flight (the one-token version sat at ~43% of DRAM bandwidth).
+// One warp per kTokPerWarp consecutive tokens. The first slice of every row
+// is loaded before the destinations are resolved (group -> tile offset ->
+// base is a chain of dependent loads), so row traffic overlaps the index
+// work; then each 32*kRowUnroll-vector slice is stored and the next loaded.
 __global__ void __launch_bounds__(256) permute_kernel(PermuteParams p) {
   const int warps = (gridDim.x * blockDim.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int vec = p.d >> 3;  // uint4 per row
+  const bool copy = p.x_perm != nullptr;
   for (int t0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kTokPerWarp; t0 < p.T;
        t0 += warps * kTokPerWarp) {
+    int4 v[kTokPerWarp][kRowUnroll];
+    auto load_slice = [&](int i0) {
+#pragma unroll
+      for (int u = 0; u < kTokPerWarp; ++u)
+#pragma unroll
+        for (int w = 0; w < kRowUnroll; ++w) {
+          const int i = i0 + w * 32 + lane;
+          if (copy && t0 + u < p.T && i < vec)
+            v[u][w] = ld_nc_v4(reinterpret_cast<const int4*>(p.x + static_cast<long>(t0 + u) * p.d) + i);
+        }
+    };
+    load_slice(0);
     int dst[kTokPerWarp][2];
 #pragma unroll
     for (int u = 0; u < kTokPerWarp; ++u) {
@@ -67,17 +81,6 @@ __global__ void __launch_bounds__(256) permute_kernel(PermuteParams p) {
       }
     }
     for (int i0 = 0; i0 < vec; i0 += 32 * kRowUnroll) {
-      int4 v[kTokPerWarp][kRowUnroll];
-#pragma unroll
-      for (int u = 0; u < kTokPerWarp; ++u) {
-        const bool need = (dst[u][0] >= 0 || dst[u][1] >= 0) && p.x_perm;
-#pragma unroll
-        for (int w = 0; w < kRowUnroll; ++w) {
-          const int i = i0 + w * 32 + lane;
-          if (need && i < vec)
-            v[u][w] = ld_nc_v4(reinterpret_cast<const int4*>(p.x + static_cast<long>(t0 + u) * p.d) + i);
-        }
-      }
 #pragma unroll
       for (int u = 0; u < kTokPerWarp; ++u) {
         if (t0 + u >= p.T) continue;
@@ -86,7 +89,7 @@ __global__ void __launch_bounds__(256) permute_kernel(PermuteParams p) {
         for (int w = 0; w < kRowUnroll; ++w) {
           const int i = i0 + w * 32 + lane;
           if (i >= vec) continue;
-          if (any && p.x_perm) {
+          if (any && copy) {
 #pragma unroll
             for (int j = 0; j < 2; ++j)
               if (dst[u][j] >= 0)
@@ -96,6 +99,7 @@ __global__ void __launch_bounds__(256) permute_kernel(PermuteParams p) {
           }
         }
       }
+      if (i0 + 32 * kRowUnroll < vec) load_slice(i0 + 32 * kRowUnroll);
     }
   }
 }
