@@ -62,7 +62,8 @@ class ExpertCache:
 
     def __init__(self, host_experts: torch.Tensor, layer: int, n_slots: int,
                  workspace_slots: int = 2, policy: OffloadPolicy = None, freqs=None,
-                 pinned=(), device=None, substitution=False, similarity=None):
+                 pinned=(), device=None, substitution=False, similarity=None,
+                 priorities: dict = None, priority_threshold: float = 1.0):
         if not host_experts.is_pinned():
             raise ValueError("host expert store must be pinned memory")
         E, numel = host_experts.shape
@@ -77,6 +78,8 @@ class ExpertCache:
         self.policy = policy or OffloadPolicy()
         self.substitution = substitution
         self.similarity = similarity  # callable (eid_a, eid_b) -> float
+        self.priorities = priorities or {}
+        self.prio_threshold = priority_threshold
         self.copy_stream = torch.cuda.Stream(self.dev)
         self.ready = [torch.cuda.Event() for _ in range(n_slots)]   # slot filled
         self.free_ev = [torch.cuda.Event() for _ in range(n_slots)]  # slot's last reader done
@@ -195,7 +198,8 @@ class ExpertCache:
                 continue
             if self.substitution and self.similarity is not None:
                 dec = correct_misprediction(eid, self.state, self.similarity, self.policy,
-                                            priority=self.importance.get(eid, 0.0))
+                                            priority=self.priorities.get(eid, 0.0),
+                                            priority_threshold=self.prio_threshold)
                 if dec.action == "substitute":
                     self.stats.substitutions += 1
                     self.state.record_access(dec.expert, self.tick)
@@ -243,6 +247,70 @@ class ExpertCache:
         self.state.check_invariants()
         assert len(self.slot_of) == len(self.state.workspace) + len(self.state.cache)
         assert len(set(self.slot_of.values())) == len(self.slot_of)
+
+
+def resident_budget(variant_expert_bytes: float, cache_mode: str, cache_fraction: float,
+                    total_expert_bytes: float, cache_bytes: float = None,
+                    offload: bool = True) -> float:
+    """GPU bytes kept resident for a variant's experts (simulator.py:275-286):
+    fraction of the variant, fraction of the whole model, or absolute bytes,
+    never more than the variant itself."""
+    if not offload:
+        return variant_expert_bytes
+    if cache_mode == "fraction_of_variant":
+        budget = cache_fraction * variant_expert_bytes
+    elif cache_mode == "fraction_of_model":
+        budget = cache_fraction * total_expert_bytes
+    elif cache_mode == "absolute":
+        budget = float(cache_bytes)
+    else:
+        raise ValueError(f"unknown cache_mode {cache_mode!r}")
+    return min(budget, variant_expert_bytes)
+
+
+def required_bytes_fn(cache_mode: str, cache_fraction: float, total_expert_bytes: float,
+                      m_other: float, workspace_bytes: float, cache_bytes: float = None):
+    """select_variant's resident-bytes requirement (simulator.py:289-293)."""
+    def req(variant):
+        return resident_budget(variant.expert_bytes, cache_mode, cache_fraction,
+                               total_expert_bytes, cache_bytes) + m_other + workspace_bytes
+    return req
+
+
+def activate_variant(variant, layer: int, stats, host_experts: torch.Tensor, budget_bytes: float,
+                     workspace_slots: int = 2, top_k: int = 1, policy: OffloadPolicy = None,
+                     pin_decoder_layers=(), bandwidth: float = 55e9, substitution=False,
+                     similarity=None, device=None) -> "ExpertCache":
+    """Cache runtime for one layer of a variant, sized and seeded like
+    _Run._activate_variant (simulator.py:370-441): importance = merged
+    frequency / max, workspace = workspace_slots*K experts (capped by the
+    budget), cache = the rest of the budget, decoder layers pinned, offload
+    priorities with the priority-quantile threshold for substitution.
+    `host_experts` holds the variant's retained experts of this layer in
+    ascending principal order (row i <-> principal i of group_table)."""
+    from .aggregation import variant_freqs
+    from .offload import offload_priority
+    policy = policy or OffloadPolicy()
+    principals = sorted(variant.retained[layer])
+    freqs_all = variant_freqs(variant, stats)
+    freqs = {(layer, i): freqs_all[(layer, p)] for i, p in enumerate(principals)}
+    numel = host_experts.shape[1]
+    ebytes = float(numel * host_experts.element_size())
+    ws_cap = min(workspace_slots * top_k * ebytes, budget_bytes)
+    n_slots = int(budget_bytes // ebytes)
+    ws_slots = max(1, int(ws_cap // ebytes))
+    if n_slots <= ws_slots:
+        raise InfeasibleError(f"budget {budget_bytes:.3e} B holds {n_slots} experts; need more than "
+                              f"the {ws_slots}-expert workspace")
+    pinned = {(layer, i) for i in range(len(principals))} if layer in set(pin_decoder_layers) else set()
+    est = ebytes / max(bandwidth, 1.0)
+    prios = {e: offload_priority(f, ebytes, est, policy.gamma_prio, ebytes / est)
+             for e, f in freqs.items()}
+    thr = float(np.quantile(np.array(sorted(prios.values())), policy.priority_quantile)) if prios else 1.0
+    return ExpertCache(host_experts, layer=layer, n_slots=n_slots, workspace_slots=ws_slots,
+                       policy=policy, freqs=freqs, pinned=pinned, device=device,
+                       substitution=substitution, similarity=similarity, priorities=prios,
+                       priority_threshold=thr)
 
 
 class CachedMoELayer:

@@ -101,3 +101,38 @@ def test_cached_stack_predictive_prefetch():
     assert len(stack.prefetch_log) == 1
     for sl in layers:
         sl.layer.cache.check()
+
+
+def test_activate_variant_cache_for_fused_layer():
+    """_activate_variant-style cache for a fused (8 -> 4) variant: the cached
+    layer reproduces the all-resident merged layer bit for bit."""
+    from paper_2508_09208_b200 import ExpertPool, MoELayer, kernels
+    from paper_2508_09208_b200 import aggregation as A
+    from paper_2508_09208_b200.cache import CachedMoELayer, activate_variant
+    from paper_2508_09208_b200.moe import (Expert, MoeModel, MoeModelSpec,
+                                           cosine_only_calibration, stats_from_routing)
+    T, d, d_ff, E = 2048, 256, 512, 8
+    g = torch.Generator().manual_seed(21)
+    x = torch.randn(T, d, generator=g).to(torch.bfloat16).cuda()
+    wg = (torch.randn(d, E, generator=g) / math.sqrt(d)).cuda()
+    numel = kernels.expert_numel(d, d_ff, kernels.ACT_RELU)
+    pool = ExpertPool(E + 4, numel)
+    for s in range(E):
+        pool.view(pool.alloc()).copy_((torch.randn(numel, generator=g) * 0.02).to(torch.bfloat16).cuda())
+    layer = MoELayer(wg, pool, d_ff, capacity_factor=1.25)
+    stats = stats_from_routing({1: layer.route(x).gate.expert_idx}, E)
+    spec = MoeModelSpec(1, (1,), (), E, float(pool.slot_bytes), 1, numel)
+    model = MoeModel(spec, {(1, s): Expert(1, s, pool.view(s), float(pool.slot_bytes)) for s in range(E)})
+    var = A.fuse_model(model, stats, A.FusionConfig(mode="fixed", r=0.5), 1.0,
+                       cosine_only_calibration(), pool=pool)
+    layer.use_variant(var, 1)
+    y_ref = layer.forward(x).clone()
+    lut, principals = var.group_table(1, E)
+    host = torch.stack([var.retained[1][p].params.cpu() for p in principals]).contiguous().pin_memory()
+    cache = activate_variant(var, 1, stats, host, budget_bytes=3 * pool.slot_bytes, workspace_slots=1)
+    cl = CachedMoELayer(wg, cache, d_ff, capacity_factor=1.25)
+    cl.layer.set_variant(lut, list(range(len(principals))))
+    y = cl.forward(x)
+    torch.cuda.synchronize()
+    assert torch.equal(y, y_ref)
+    assert cache.prio_threshold <= 1.0 and len(cache.priorities) == len(principals)

@@ -139,3 +139,18 @@ def test_fusion_config_validation_and_selection():
         A.select_variant(lib, 1)
     with pytest.raises(ConfigError):
         A.VariantLibrary([mk("a", 1, 1), mk("a", 2, 1)])
+
+
+def test_resident_budget_modes_match_simulator_rules():
+    """_resident_budget / _required_fn (simulator.py:275-293), hand cases."""
+    from paper_2508_09208_b200.cache import required_bytes_fn, resident_budget
+    assert resident_budget(10.0, "fraction_of_variant", 0.5, 100.0) == 5.0
+    assert resident_budget(10.0, "fraction_of_model", 0.3, 100.0) == 10.0   # capped by the variant
+    assert resident_budget(50.0, "fraction_of_model", 0.3, 100.0) == 30.0
+    assert resident_budget(50.0, "absolute", 0.0, 100.0, cache_bytes=7.0) == 7.0
+    assert resident_budget(50.0, "absolute", 0.0, 100.0, cache_bytes=70.0, offload=False) == 50.0
+    with pytest.raises(ValueError):
+        resident_budget(1.0, "bogus", 0.5, 1.0)
+    v = A.ModelVariant("x", {}, {}, {}, 0.0, 1.0, expert_bytes=40.0)
+    req = required_bytes_fn("fraction_of_variant", 0.5, 100.0, m_other=3.0, workspace_bytes=2.0)
+    assert req(v) == 25.0
