@@ -319,9 +319,12 @@ class CachedMoELayer:
     def __init__(self, wg, cache: ExpertCache, d_ff: int, act="relu", top_k=1, norm_topk=None,
                  capacity_factor=1.25, wave_slots: int = None):
         self.cache = cache
-        self.E = cache.E
+        n_exp = wg.shape[1]
+        # group g of the layer <-> cache expert (layer, g); set_variant(lut, ...) maps a
+        # fused variant's original experts onto the cache's retained experts
         self.layer = MoELayer(wg, cache.pool, d_ff, act=act, top_k=top_k, norm_topk=norm_topk,
-                              capacity_factor=capacity_factor, expert_slots=[0] * cache.E)
+                              capacity_factor=capacity_factor, expert_slots=[0] * n_exp)
+        self.E = max(n_exp, cache.E)
         free = cache.pool.n_slots - len(cache.hard_pinned)
         # half the free slots per wave: wave k+1 can stream in while wave k computes
         self.wave_slots = wave_slots or max(1, free // 2)
@@ -347,6 +350,9 @@ class CachedMoELayer:
             after_route(r)
         c = self.cache
         c.tick += 1
+        if len(kept) > c.E:
+            raise ValueError(f"layer has {len(kept)} groups but the cache holds {c.E} experts; "
+                             "call layer.set_variant(lut, ...) for a fused variant")
         order = [int(g) for g in np.argsort(-kept, kind="stable") if kept[g] > 0]
         hits = [g for g in order if c.state.resident((c.layer, g))]
         misses = [g for g in order if not c.state.resident((c.layer, g))]
@@ -362,13 +368,14 @@ class CachedMoELayer:
             slots = c.serve(ids)
             c.stats.waves += 1
             tab[w] = 0
+            G = len(kept)
             for g in wave:
                 tab[w, 0, g] = kept[g]
                 tab[w, 1, g] = slots[(c.layer, g)]
             used = sorted({slots[e] for e in ids})
             self._tables_dev[w].copy_(self._tables[w], non_blocking=True)
             c.wait_ready(used, comp)
-            g_rows, g_slot = self._tables_dev[w, 0], self._tables_dev[w, 1]
+            g_rows, g_slot = self._tables_dev[w, 0, :G], self._tables_dev[w, 1, :G]
             kernels.grouped_gemm(r.perm.x_perm, c.pool.data, 0, n1, g_rows, r.scan.group_base,
                                  g_slot, epi1, ws["h"])
             kernels.grouped_gemm(ws["h"], c.pool.data, n1 * L.d, L.d, g_rows, r.scan.group_base,
