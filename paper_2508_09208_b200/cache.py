@@ -331,6 +331,14 @@ class CachedMoELayer:
         self._tables = torch.zeros((self.E, 2, self.E), dtype=torch.int32).pin_memory()
         self._tables_dev = torch.zeros((self.E, 2, self.E), dtype=torch.int32, device=wg.device)
 
+    def set_groups(self, slot_map) -> None:
+        """Route through a fused variant: slot_map[E] -> group index, where
+        group g is the cache's expert (layer, g) (ModelVariant.group_table)."""
+        G = max(slot_map) + 1
+        if G > self.cache.E:
+            raise ValueError(f"{G} groups but the cache holds {self.cache.E} experts")
+        self.layer.set_variant(slot_map, [0] * G)  # slots come from the cache per wave
+
     def forward(self, x, out=None, after_route=None):
         """`after_route(routing)` runs after the demand set is known and before
         the GEMMs are enqueued: the stack issues the next layer's prefetch

@@ -131,7 +131,7 @@ def test_activate_variant_cache_for_fused_layer():
     host = torch.stack([var.retained[1][p].params.cpu() for p in principals]).contiguous().pin_memory()
     cache = activate_variant(var, 1, stats, host, budget_bytes=3 * pool.slot_bytes, workspace_slots=1)
     cl = CachedMoELayer(wg, cache, d_ff, capacity_factor=1.25)
-    cl.layer.set_variant(lut, list(range(len(principals))))
+    cl.set_groups(lut)
     y = cl.forward(x)
     torch.cuda.synchronize()
     assert torch.equal(y, y_ref)
