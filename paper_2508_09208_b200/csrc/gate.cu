@@ -113,7 +113,8 @@ __global__ void __launch_bounds__(kGateThreads, 1)
 
   if (warp == 0) {
     if (elect_one()) {
-      const uint64_t pol_x = l2_policy_evict_first();
+      // keep x in L2: the permute re-reads every row right after the gate
+      const uint64_t pol_x = l2_policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
