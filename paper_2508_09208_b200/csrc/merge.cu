@@ -38,25 +38,42 @@ __global__ void __launch_bounds__(256) merge_bf16_kernel(const void* const* __re
   int4* dst = reinterpret_cast<int4*>(outs[g]);
   const long nvec = D >> 3;
   const long stride = static_cast<long>(gridDim.x) * blockDim.x;
-  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < nvec; i += stride) {
-    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  // two 16-byte vectors per thread per member in flight (i and i + stride)
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < nvec;
+       i += 2 * stride) {
+    const long i2 = i + stride;
+    const bool two = i2 < nvec;
+    float acc[2][8];
+#pragma unroll
+    for (int v = 0; v < 2; ++v)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc[v][u] = 0.f;
     for (int j = 0; j < n; ++j) {
-      const int4 raw = ld_nc_v4(src[j] + i);
-      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+      const int4 r0 = ld_nc_v4(src[j] + i);
+      const int4 r1 = two ? ld_nc_v4(src[j] + i2) : make_int4(0, 0, 0, 0);
       const float wj = w[j];
+      const __nv_bfloat162* h0 = reinterpret_cast<const __nv_bfloat162*>(&r0);
+      const __nv_bfloat162* h1 = reinterpret_cast<const __nv_bfloat162*>(&r1);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const float2 f = __bfloat1622float2(h[u]);
-        acc[2 * u] = fmaf(wj, f.x, acc[2 * u]);
-        acc[2 * u + 1] = fmaf(wj, f.y, acc[2 * u + 1]);
+        const float2 f0 = __bfloat1622float2(h0[u]);
+        const float2 f1 = __bfloat1622float2(h1[u]);
+        acc[0][2 * u] = fmaf(wj, f0.x, acc[0][2 * u]);
+        acc[0][2 * u + 1] = fmaf(wj, f0.y, acc[0][2 * u + 1]);
+        acc[1][2 * u] = fmaf(wj, f1.x, acc[1][2 * u]);
+        acc[1][2 * u + 1] = fmaf(wj, f1.y, acc[1][2 * u + 1]);
       }
     }
-    int4 o;
-    o.x = static_cast<int>(pack_bf16x2(acc[0], acc[1]));
-    o.y = static_cast<int>(pack_bf16x2(acc[2], acc[3]));
-    o.z = static_cast<int>(pack_bf16x2(acc[4], acc[5]));
-    o.w = static_cast<int>(pack_bf16x2(acc[6], acc[7]));
-    dst[i] = o;
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      if (v == 1 && !two) break;
+      int4 o;
+      o.x = static_cast<int>(pack_bf16x2(acc[v][0], acc[v][1]));
+      o.y = static_cast<int>(pack_bf16x2(acc[v][2], acc[v][3]));
+      o.z = static_cast<int>(pack_bf16x2(acc[v][4], acc[v][5]));
+      o.w = static_cast<int>(pack_bf16x2(acc[v][6], acc[v][7]));
+      dst[v ? i2 : i] = o;
+    }
   }
 }
 

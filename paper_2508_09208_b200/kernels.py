@@ -279,16 +279,28 @@ def merge_groups(groups_members, weights, divisors, outs, dtype) -> None:
         if o.numel() != D:
             raise ValueError("output size mismatch")
     max_members = max(offs[i + 1] - offs[i] for i in range(len(outs)))
-    t_ptrs = torch.tensor(ptrs, dtype=torch.int64).to(dev, non_blocking=False)
-    t_offs = torch.tensor(offs, dtype=torch.int32).to(dev)
-    t_w = torch.tensor(ws, dtype=torch.float64).to(dev)
-    t_div = torch.tensor([float(x) for x in divisors], dtype=torch.float64).to(dev)
-    t_out = torch.tensor([o.data_ptr() for o in outs], dtype=torch.int64).to(dev)
+    # one pinned staging buffer, one async H2D: [ptrs | outs | offs | weights | divisors]
+    nm, ng = len(ptrs), len(outs)
+    host = torch.empty(nm + ng + (ng + 2) // 2 + nm + ng, dtype=torch.int64).pin_memory()
+    host[:nm] = torch.tensor(ptrs, dtype=torch.int64)
+    host[nm:nm + ng] = torch.tensor([o.data_ptr() for o in outs], dtype=torch.int64)
+    o_off = nm + ng
+    n_off_words = (ng + 2) // 2
+    host[o_off:o_off + n_off_words].view(torch.int32)[:ng + 1] = torch.tensor(offs, dtype=torch.int32)
+    w_off = o_off + n_off_words
+    host[w_off:w_off + nm].view(torch.float64)[:] = torch.tensor(ws, dtype=torch.float64)
+    host[w_off + nm:].view(torch.float64)[:] = torch.tensor([float(x) for x in divisors],
+                                                           dtype=torch.float64)
+    dev_tab = host.to(dev, non_blocking=True)
+    t_ptrs, t_out = dev_tab[:nm], dev_tab[nm:nm + ng]
+    t_offs = dev_tab[o_off:o_off + n_off_words].view(torch.int32)
+    t_w = dev_tab[w_off:w_off + nm].view(torch.float64)
+    t_div = dev_tab[w_off + nm:].view(torch.float64)
     _lib.call("comoe_merge", code, _ptr(t_ptrs), _ptr(t_offs), _ptr(t_w), _ptr(t_div),
               _ptr(t_out), len(outs), max_members, D, _stream())
-    # the caching allocator is stream-ordered, so the pointer tables may be
-    # released now: any reuse is enqueued after this kernel on the same stream
-    del t_ptrs, t_offs, t_w, t_div, t_out
+    # both allocators are stream-ordered: PyTorch's pinned-host allocator records
+    # the async copy before reusing `host`, and dev_tab is reused only after this
+    # kernel in stream order
 
 
 # ---------------------------------------------------------------- K6 similarity
