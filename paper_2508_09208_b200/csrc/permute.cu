@@ -34,7 +34,7 @@ constexpr int kTokPerWarp = 4;
 // is loaded before the destinations are resolved (group -> tile offset ->
 // base is a chain of dependent loads), so row traffic overlaps the index
 // work; then each 32*kRowUnroll-vector slice is stored and the next loaded.
-__global__ void __launch_bounds__(256) permute_kernel(PermuteParams p) {
+__global__ void __launch_bounds__(256, 3) permute_kernel(PermuteParams p) {
   const int warps = (gridDim.x * blockDim.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int vec = p.d >> 3;  // uint4 per row
@@ -53,30 +53,47 @@ __global__ void __launch_bounds__(256) permute_kernel(PermuteParams p) {
         }
     };
     load_slice(0);
+    // index chain in two independent phases over all tokens of the warp
+    // (group/local rank, then tile offset/base), instead of serially per token
+    int g[kTokPerWarp][2], lr[kTokPerWarp][2];
+#pragma unroll
+    for (int u = 0; u < kTokPerWarp; ++u)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const bool ok = t0 + u < p.T && j < p.top_k;
+        const long o = static_cast<long>(t0 + u) * p.top_k + j;
+        g[u][j] = ok ? __ldg(p.group_idx + o) : -1;
+        lr[u][j] = ok ? __ldg(p.local_rank + o) : 0;
+      }
     int dst[kTokPerWarp][2];
 #pragma unroll
-    for (int u = 0; u < kTokPerWarp; ++u) {
-      const int t = t0 + u;
-      dst[u][0] = dst[u][1] = -1;
-      if (t >= p.T) continue;
-      const int tile = t / 128;
-      for (int j = 0; j < p.top_k; ++j) {
-        const long o = static_cast<long>(t) * p.top_k + j;
-        const int g = __ldg(p.group_idx + o);
+    for (int u = 0; u < kTokPerWarp; ++u)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int gg = g[u][j];
         int dest = -1;
-        if (g >= 0) {
+        if (gg >= 0) {
+          const int tile = (t0 + u) / 128;
           const int rank =
-              __ldg(p.tile_offset + (static_cast<long>(j) * p.ntiles + tile) * p.G + g) +
-              __ldg(p.local_rank + o);
-          if (rank < p.capacity) dest = __ldg(p.group_base + g) + rank;
+              __ldg(p.tile_offset + (static_cast<long>(j) * p.ntiles + tile) * p.G + gg) + lr[u][j];
+          if (rank < p.capacity) dest = __ldg(p.group_base + gg) + rank;
         }
         dst[u][j] = dest;
-        if (lane == 0) {
-          p.token_pos[o] = dest;
-          if (dest >= 0) {
-            p.row_token[dest] = t;
-            p.row_prob[dest] = __ldg(p.gate_prob + o);
-          }
+      }
+    if (lane < kTokPerWarp * 2) {  // one lane per (token, choice) writes the tables
+      const int u = lane >> 1, j = lane & 1;
+      int dest = -1, t = t0 + u;
+#pragma unroll
+      for (int uu = 0; uu < kTokPerWarp; ++uu)
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj)
+          if (uu == u && jj == j) dest = dst[uu][jj];
+      if (t < p.T && j < p.top_k) {
+        const long o = static_cast<long>(t) * p.top_k + j;
+        p.token_pos[o] = dest;
+        if (dest >= 0) {
+          p.row_token[dest] = t;
+          p.row_prob[dest] = __ldg(p.gate_prob + o);
         }
       }
     }
