@@ -12,6 +12,8 @@
 // router weight is split Wg = hi + mid + lo with each term bf16, so every
 // product x*term is exact in the fp32 accumulator and the three MMAs sum to
 // the fp32 logit up to accumulation rounding.
+#include <cooperative_groups.h>
+
 #include "grouped_gemm.cuh"
 #include "../../include/comoe_b200.h"
 
@@ -352,6 +354,55 @@ __global__ void route_scan_columns(const int* __restrict__ hist, int n_rows, int
   if (threadIdx.x == 0) count[g] = carry;
 }
 
+// One cooperative launch (block g = group g): column scan -> grid sync ->
+// kept[g] = min(count[g], C), base[g] = sum_{h<g} kept[h] (each block sums
+// the earlier groups' kept counts itself). Replaces columns + bases.
+__global__ void __launch_bounds__(256) route_scan_coop(const int* __restrict__ hist, int n_rows,
+                                                       int G, int capacity,
+                                                       int* __restrict__ offset,
+                                                       int* __restrict__ count,
+                                                       int* __restrict__ kept,
+                                                       int* __restrict__ base) {
+  __shared__ int warp_tot[32];
+  const int g = blockIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int carry = 0;
+  for (int b0 = 0; b0 < n_rows; b0 += blockDim.x) {
+    const int r = b0 + threadIdx.x;
+    const int x = r < n_rows ? hist[static_cast<long>(r) * G + g] : 0;
+    int v = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int n = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += n;
+    }
+    if (lane == 31) warp_tot[w] = v;
+    __syncthreads();
+    int wb = 0, tot = 0;
+    for (int i = 0; i < nw; ++i) {
+      if (i < w) wb += warp_tot[i];
+      tot += warp_tot[i];
+    }
+    if (r < n_rows) offset[static_cast<long>(r) * G + g] = carry + wb + v - x;
+    carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) count[g] = carry;
+  cooperative_groups::this_grid().sync();
+  int part = 0;
+  for (int h = threadIdx.x; h < g; h += blockDim.x) part += min(__ldcg(count + h), capacity);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  if (lane == 0) warp_tot[w] = part;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int sum = 0;
+    for (int i = 0; i < nw; ++i) sum += warp_tot[i];
+    kept[g] = min(carry, capacity);
+    base[g] = sum;
+  }
+}
+
 // kept = min(count, C); base = exclusive scan of kept.
 __global__ void route_scan_bases(const int* __restrict__ count, int G, int capacity,
                                  int* __restrict__ kept, int* __restrict__ base) {
@@ -555,6 +606,22 @@ int comoe_route_scan(const int* tile_hist, int top_k, int ntiles, int G, int cap
   COMOE_REQUIRE(G >= 1 && G <= 32 * 1024, kBadArg, "route_scan: G=%d", G);
   COMOE_REQUIRE(capacity >= 0, kBadArg, "route_scan: capacity=%d", capacity);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  static int coop_blocks = -1;  // co-resident capacity of the cooperative scan
+  if (coop_blocks < 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, route_scan_coop, 256, 0);
+    coop_blocks = sms * per_sm;
+  }
+  if (G <= coop_blocks) {
+    int n_rows = top_k * ntiles;
+    void* args[] = {const_cast<int**>(&tile_hist), &n_rows, &G, &capacity, &tile_offset,
+                    &group_count, &group_kept, &group_base};
+    cudaLaunchCooperativeKernel(reinterpret_cast<void*>(route_scan_coop), dim3(G), dim3(256),
+                                args, 0, s);
+    return check_launch("route_scan_coop");
+  }
   route_scan_columns<<<G, 256, 0, s>>>(tile_hist, top_k * ntiles, G, tile_offset, group_count);
   int rc = check_launch("route_scan_columns");
   if (rc) return rc;

@@ -156,5 +156,5 @@ class EPMoELayer:
 
     @property
     def kernels_per_forward(self) -> int:
-        # gate, 2x scan, permute, 2x GEMM, combine (NCCL's all-to-all kernels not counted)
-        return 7
+        # gate, scan, permute, 2x GEMM, combine (NCCL's all-to-all kernels not counted)
+        return 6

@@ -213,5 +213,5 @@ class MoELayer:
 
     @property
     def kernels_per_forward(self) -> int:
-        """Device kernels one forward launches (gate, 2x scan, permute, 2x GEMM [, combine])."""
-        return 6 + (0 if self.top_k == 1 else 1)
+        """Device kernels one forward launches (gate, scan, permute, 2x GEMM [, combine])."""
+        return 5 + (0 if self.top_k == 1 else 1)
