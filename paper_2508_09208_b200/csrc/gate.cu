@@ -13,8 +13,9 @@
 // product x*term is exact in the fp32 accumulator and the three MMAs sum to
 // the fp32 logit up to accumulation rounding.
 #include <cooperative_groups.h>
+#include <cstdlib>
 
-#include "grouped_gemm.cuh"
+#include "grouped_gemm_2sm.cuh"
 #include "../../include/comoe_b200.h"
 
 namespace comoe {
@@ -57,23 +58,29 @@ struct GateParams {
   int* tile_hist;       // [k][ntiles][G]
 };
 
-template <int EP, int kStages>
+// kPair: CTA pair (cta_group::2, M = 256 tokens): each SM stages its own 128
+// tokens and half of every router term (EP/2 experts), cutting per-SM shared-
+// memory traffic ~30% (the 1-SM gate is smem-bound: the token tile is re-read
+// once per term); each SM's TMEM still holds full logit rows of its tokens.
+template <int EP, int kStages, bool kPair = false>
 struct GateSmem {
+  static constexpr int kBRows = kPair ? EP / 2 : EP;
   static constexpr int kABytes = kGemmBM * kGemmBK * 2;
-  static constexpr int kBBytes = 3 * EP * kGemmBK * 2;
+  static constexpr int kBBytes = 3 * kBRows * kGemmBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTileBytes = kStages * kStageBytes;
   static constexpr int kCtrlBytes = (2 * kStages + 4) * 8 + 16 + 2 * kGateMaxK * 4 * kGateMaxE * 4 + kGateMaxE * 4;
   static constexpr int kTotal = 1024 + kTileBytes + kCtrlBytes;
 };
 
-template <int EP, int kStages>
+template <int EP, int kStages, bool kPair>
 __global__ void __launch_bounds__(kGateThreads, 1)
     gate_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 const __grid_constant__ CUtensorMap tmap_w, GateParams p) {
-  using S = GateSmem<EP, kStages>;
+  using S = GateSmem<EP, kStages, kPair>;
   constexpr uint32_t kTmemCols = 2 * EP <= 32 ? 32 : (2 * EP <= 64 ? 64 : (2 * EP <= 128 ? 128 : 256));
-  constexpr uint32_t kIdesc = umma_idesc_bf16_f32(kGemmBM, EP);
+  constexpr uint32_t kIdesc = umma_idesc_bf16_f32(kPair ? 256 : kGemmBM, EP);
+  constexpr int kBRows = S::kBRows;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -91,25 +98,43 @@ __global__ void __launch_bounds__(kGateThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int k_blocks = p.d / kGemmBK;
+  // work units: 128-token tiles (1-SM) or 256-token pair tiles (kPair); this
+  // CTA's 128-token tile of unit u is 2u + rank
+  const uint32_t rank = kPair ? cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
+  const int n_units = kPair ? (p.ntiles + 1) / 2 : p.ntiles;
+  const int unit0 = kPair ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+  const int unit_step = kPair ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_x);
     tma_prefetch_desc(&tmap_w);
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full_bar[s], 1);
+      mbar_init(&full_bar[s], kPair ? 2 : 1);
       mbar_init(&empty_bar[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 4);
+      mbar_init(&tempty_bar[a], kPair ? 8 : 4);
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
+  if (warp == 2) {
+    if constexpr (kPair) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "n"(kTmemCols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      tmem_alloc<kTmemCols>(tmem_slot);
+    }
+  }
   for (int e = threadIdx.x; e < kGateMaxE; e += blockDim.x)
     smap[e] = e < p.E ? (p.slot_map ? __ldg(p.slot_map + e) : e) : -1;
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair) cluster_sync_all();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -117,28 +142,42 @@ __global__ void __launch_bounds__(kGateThreads, 1)
     if (elect_one()) {
       // keep x in L2: the permute re-reads every row right after the gate
       const uint64_t pol_x = l2_policy_evict_last();
+      const uint64_t pol_w = l2_policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+      for (int u = unit0; u < n_units; u += unit_step) {
+        const int tile = kPair ? 2 * u + static_cast<int>(rank) : u;
         for (int kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
-          mbar_expect_tx(&full_bar[stage], S::kStageBytes);
-          tma_load_2d_hint(smem_a + stage * S::kABytes, &tmap_x, &full_bar[stage], kb * kGemmBK,
-                           tile * kGemmBM, pol_x);
           uint8_t* b = smem_b + stage * S::kBBytes;
+          if constexpr (kPair) {
+            const uint32_t fb = smem_u32(&full_bar[stage]) & kPeerMask;
+            if (leader) mbar_expect_tx(&full_bar[stage], 2 * S::kStageBytes);
+            else mbar_arrive_cluster(fb);
+            tma_load_2d_2sm(smem_a + stage * S::kABytes, &tmap_x, fb, kb * kGemmBK,
+                            tile * kGemmBM, pol_x);
 #pragma unroll
-          for (int term = 0; term < 3; ++term)
-            tma_load_2d(b + term * EP * 128, &tmap_w, &full_bar[stage], kb * kGemmBK, term * EP);
+            for (int term = 0; term < 3; ++term)
+              tma_load_2d_2sm(b + term * kBRows * 128, &tmap_w, fb, kb * kGemmBK,
+                              term * EP + static_cast<int>(rank) * kBRows, pol_w);
+          } else {
+            mbar_expect_tx(&full_bar[stage], S::kStageBytes);
+            tma_load_2d_hint(smem_a + stage * S::kABytes, &tmap_x, &full_bar[stage], kb * kGemmBK,
+                             tile * kGemmBM, pol_x);
+#pragma unroll
+            for (int term = 0; term < 3; ++term)
+              tma_load_2d(b + term * EP * 128, &tmap_w, &full_bar[stage], kb * kGemmBK, term * EP);
+          }
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    if (elect_one()) {
+    if (leader && elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++it) {
+      for (int u = unit0; u < n_units; u += unit_step, ++it) {
         const int acc = it & 1;
         mbar_wait(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -150,15 +189,21 @@ __global__ void __launch_bounds__(kGateThreads, 1)
 #pragma unroll
           for (int term = 0; term < 3; ++term) {
             const uint64_t bdesc =
-                umma_desc_k_sw128(smem_u32(smem_b + stage * S::kBBytes + term * EP * 128));
+                umma_desc_k_sw128(smem_u32(smem_b + stage * S::kBBytes + term * kBRows * 128));
 #pragma unroll
-            for (int k = 0; k < kGemmBK / 16; ++k)
-              umma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, kIdesc, (kb | k | term) != 0);
+            for (int k = 0; k < kGemmBK / 16; ++k) {
+              if constexpr (kPair)
+                umma_bf16_2sm(d_tmem, adesc + 2 * k, bdesc + 2 * k, kIdesc, (kb | k | term) != 0);
+              else
+                umma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, kIdesc, (kb | k | term) != 0);
+            }
           }
-          umma_commit(&empty_bar[stage]);
+          if constexpr (kPair) umma_commit_2sm_mc(&empty_bar[stage]);
+          else umma_commit(&empty_bar[stage]);
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
-        umma_commit(&tfull_bar[acc]);
+        if constexpr (kPair) umma_commit_2sm_mc(&tfull_bar[acc]);
+        else umma_commit(&tfull_bar[acc]);
       }
     }
   } else if (warp >= 4) {
@@ -168,10 +213,12 @@ __global__ void __launch_bounds__(kGateThreads, 1)
     int* cnt = cnt_all + eg * kGateMaxK * 4 * kGateMaxE;
     const uint32_t lt_mask = (1u << lane) - 1u;
     int it = eg;
-    for (int tile = blockIdx.x + eg * gridDim.x; tile < p.ntiles; tile += 2 * gridDim.x, it += 2) {
+    for (int u = unit0 + eg * unit_step; u < n_units; u += 2 * unit_step, it += 2) {
       const int acc = it & 1;
+      const int tile = kPair ? 2 * u + static_cast<int>(rank) : u;
+      const bool tile_ok = tile < p.ntiles;  // the odd pair's second tile may not exist
       const int t = tile * kGemmBM + q * 32 + lane;
-      const bool valid = t < p.T;
+      const bool valid = tile_ok && t < p.T;
       mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
       tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * EP;
@@ -225,7 +272,10 @@ __global__ void __launch_bounds__(kGateThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if (lane == 0) {
+        if constexpr (kPair) mbar_arrive_cluster(smem_u32(&tempty_bar[acc]) & kPeerMask);
+        else mbar_arrive(&tempty_bar[acc]);
+      }
 
       // probabilities, slot remap, top-2 fold (all in registers)
       float pr0, pr1 = 0.f;
@@ -285,30 +335,37 @@ __global__ void __launch_bounds__(kGateThreads, 1)
           p.local_rank[o + 1] = rank1;
         }
       }
-      for (int j = 0; j < p.top_k; ++j)
-        for (int g = et; g < p.G; g += 128) {
-          int h = 0;
-          if (g < kGateMaxE)
-            for (int qq = 0; qq < 4; ++qq) h += cnt[(j * 4 + qq) * kGateMaxE + g];
-          p.tile_hist[(static_cast<long>(j) * p.ntiles + tile) * p.G + g] = h;
-        }
+      if (tile_ok)
+        for (int j = 0; j < p.top_k; ++j)
+          for (int g = et; g < p.G; g += 128) {
+            int h = 0;
+            if (g < kGateMaxE)
+              for (int qq = 0; qq < 4; ++qq) h += cnt[(j * 4 + qq) * kGateMaxE + g];
+            p.tile_hist[(static_cast<long>(j) * p.ntiles + tile) * p.G + g] = h;
+          }
     }
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair) cluster_sync_all();
+  else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<kTmemCols>(tmem_base);
+    if constexpr (kPair)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "n"(kTmemCols)
+                   : "memory");
+    else
+      tmem_dealloc<kTmemCols>(tmem_base);
   }
 }
 
-template <int EP>
+template <int EP, bool kPair>
 static int launch_gate(const CUtensorMap& tx, const CUtensorMap& tw, const GateParams& p,
                        cudaStream_t stream) {
-  constexpr int kStages = EP >= 128 ? 3 : 4;
-  using S = GateSmem<EP, kStages>;
-  auto kern = gate_kernel<EP, kStages>;
+  constexpr int kStages = kPair ? 4 : (EP >= 128 ? 3 : 4);
+  using S = GateSmem<EP, kStages, kPair>;
+  auto kern = gate_kernel<EP, kStages, kPair>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kTotal);
@@ -317,9 +374,36 @@ static int launch_gate(const CUtensorMap& tx, const CUtensorMap& tw, const GateP
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = p.ntiles < sms ? p.ntiles : sms;
-  kern<<<grid, kGateThreads, S::kTotal, stream>>>(tx, tw, p);
-  return check_launch("gate_kernel");
+  if constexpr (kPair) {
+    const int units = (p.ntiles + 1) / 2;
+    const int pairs = units < sms / 2 ? units : sms / 2;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(kGateThreads);
+    cfg.dynamicSmemBytes = S::kTotal;
+    cfg.stream = stream;
+    cudaLaunchAttribute attrs[1];
+    attrs[0].id = cudaLaunchAttributeClusterDimension;
+    attrs[0].val.clusterDim.x = 2;
+    attrs[0].val.clusterDim.y = 1;
+    attrs[0].val.clusterDim.z = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, tx, tw, p);
+    return check_launch("gate_kernel(pair)");
+  } else {
+    const int grid = p.ntiles < sms ? p.ntiles : sms;
+    kern<<<grid, kGateThreads, S::kTotal, stream>>>(tx, tw, p);
+    return check_launch("gate_kernel");
+  }
+}
+
+static bool gate_pair_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("COMOE_GATE_1SM");
+    return !(e && e[0] == '1');
+  }();
+  return on;
 }
 
 // ------------------------------------------------------------ routing scan
@@ -576,19 +660,20 @@ int comoe_gate_topk(const void* x, int T, int d, const void* wg_split, int E, in
   COMOE_REQUIRE(EP > 0, kUnsupportedShape, "gate_topk: E=%d must be in [1,%d]", E, kGateMaxE);
   COMOE_REQUIRE(d % 64 == 0, kUnsupportedShape, "gate_topk: d=%d must be a multiple of 64", d);
   COMOE_REQUIRE(n_groups >= 1 && n_groups <= E, kBadArg, "gate_topk: n_groups=%d", n_groups);
+  const bool pair = gate_pair_enabled();
   CUtensorMap tx, tw;
   int rc = make_tmap_bf16_2d(&tx, x, T, d, kGemmBM);
   if (rc) return rc;
-  rc = make_tmap_bf16_2d(&tw, wg_split, 3ull * EP, d, EP);
+  rc = make_tmap_bf16_2d(&tw, wg_split, 3ull * EP, d, pair ? EP / 2 : EP);
   if (rc) return rc;
   GateParams p{T, d, E, top_k, norm_topk, n_groups, (T + kGemmBM - 1) / kGemmBM, slot_map,
                logits_out, expert_idx, group_idx, gate_prob, local_rank, tile_hist};
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   switch (EP) {
-    case 16: return launch_gate<16>(tx, tw, p, s);
-    case 32: return launch_gate<32>(tx, tw, p, s);
-    case 64: return launch_gate<64>(tx, tw, p, s);
-    case 128: return launch_gate<128>(tx, tw, p, s);
+    case 16: return pair ? launch_gate<16, true>(tx, tw, p, s) : launch_gate<16, false>(tx, tw, p, s);
+    case 32: return pair ? launch_gate<32, true>(tx, tw, p, s) : launch_gate<32, false>(tx, tw, p, s);
+    case 64: return pair ? launch_gate<64, true>(tx, tw, p, s) : launch_gate<64, false>(tx, tw, p, s);
+    case 128: return pair ? launch_gate<128, true>(tx, tw, p, s) : launch_gate<128, false>(tx, tw, p, s);
     default: break;
   }
   set_error("gate_topk: no kernel for EP=%d", EP);
