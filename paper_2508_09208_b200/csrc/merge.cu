@@ -12,7 +12,8 @@
 // separately, rows summed in member order, one final division — no FMA
 // contraction — so results are bit-identical to the reference.
 // bf16 mode streams 16-byte vectors with fp32 accumulation (w_j/divisor
-// pre-divided in fp64), reading each member once and writing the merge once.
+// divided in fp64, then rounded to fp32), reading each member once and
+// writing the merge once.
 #include "common.cuh"
 #include "../../include/comoe_b200.h"
 
@@ -20,53 +21,91 @@ namespace comoe {
 
 constexpr int kMergeMaxMembers = 64;
 
-__global__ void __launch_bounds__(256) merge_bf16_kernel(const void* const* __restrict__ members,
-                                                         const int* __restrict__ offsets,
-                                                         const double* __restrict__ weights,
-                                                         const double* __restrict__ divisor,
-                                                         void* const* __restrict__ outs, long D) {
-  const int g = blockIdx.y;
-  const int m0 = offsets[g], m1 = offsets[g + 1];
-  const int n = m1 - m0;
-  __shared__ float w[kMergeMaxMembers];
-  __shared__ const int4* src[kMergeMaxMembers];
-  if (threadIdx.x < n) {
-    w[threadIdx.x] = static_cast<float>(weights[m0 + threadIdx.x] / divisor[g]);
-    src[threadIdx.x] = reinterpret_cast<const int4*>(members[m0 + threadIdx.x]);
-  }
-  __syncthreads();
-  int4* dst = reinterpret_cast<int4*>(outs[g]);
+// Work item = (group, 512-vector chunk), items interleaved over groups
+// (item w -> group w % G) and grid-strided by a persistent grid, so groups
+// of 2..N members share the machine in proportion to their bytes (one
+// block range per group left the 5-member groups as a long tail). Each
+// thread keeps up to kMergeBatch members x 2 vectors of loads in flight.
+constexpr int kMergeBatch = 2;
+constexpr int kMergeSmemMembers = 2048;
+constexpr int kMergeSmemGroups = 1024;
+constexpr int kMergeThreads = 256;
+
+__global__ void __launch_bounds__(kMergeThreads, 4) merge_bf16_kernel(
+    const void* const* __restrict__ members, const int* __restrict__ offsets,
+    const double* __restrict__ weights, const double* __restrict__ divisor,
+    void* const* __restrict__ outs, long D, int G) {
   const long nvec = D >> 3;
-  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
-  // two 16-byte vectors per thread per member in flight (i and i + stride)
-  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < nvec;
-       i += 2 * stride) {
-    const long i2 = i + stride;
-    const bool two = i2 < nvec;
+  constexpr long kChunk = 2L * kMergeThreads;
+  const long chunks = (nvec + kChunk - 1) / kChunk;
+  const long items = chunks * G;
+  // member pointers, group offsets and normalised fp32 weights w_j / divisor_g
+  // staged in shared memory once per block: per work item only the data
+  // loads remain on the critical path (chained global loads offsets ->
+  // pointer -> data per item, plus an fp64 division per member, cost 1.5x)
+  __shared__ float wn[kMergeSmemMembers];
+  __shared__ const int4* mp[kMergeSmemMembers];
+  __shared__ int offs[kMergeSmemGroups + 1];
+  const int n_members = __ldg(offsets + G);
+  const bool staged = n_members <= kMergeSmemMembers && G <= kMergeSmemGroups;
+  if (staged) {
+    for (int g = threadIdx.x; g <= G; g += blockDim.x) offs[g] = __ldg(offsets + g);
+    __syncthreads();
+    for (int m = threadIdx.x; m < n_members; m += blockDim.x) {
+      int lo = 0, hi = G - 1;  // group of member m: largest g with offs[g] <= m
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (offs[mid] <= m) lo = mid; else hi = mid - 1;
+      }
+      wn[m] = static_cast<float>(__ldg(weights + m) / __ldg(divisor + lo));
+      mp[m] = reinterpret_cast<const int4*>(members[m]);
+    }
+    __syncthreads();
+  }
+  for (long item = blockIdx.x; item < items; item += gridDim.x) {
+    const int g = static_cast<int>(item % G);
+    const long i = (item / G) * kChunk + threadIdx.x;
+    const long i2 = i + kMergeThreads;
+    const bool one = i < nvec, two = i2 < nvec;
+    const int m0 = staged ? offs[g] : __ldg(offsets + g);
+    const int n = (staged ? offs[g + 1] : __ldg(offsets + g + 1)) - m0;
+    const double dv = staged ? 1.0 : __ldg(divisor + g);
     float acc[2][8];
 #pragma unroll
     for (int v = 0; v < 2; ++v)
 #pragma unroll
       for (int u = 0; u < 8; ++u) acc[v][u] = 0.f;
-    for (int j = 0; j < n; ++j) {
-      const int4 r0 = ld_nc_v4(src[j] + i);
-      const int4 r1 = two ? ld_nc_v4(src[j] + i2) : make_int4(0, 0, 0, 0);
-      const float wj = w[j];
-      const __nv_bfloat162* h0 = reinterpret_cast<const __nv_bfloat162*>(&r0);
-      const __nv_bfloat162* h1 = reinterpret_cast<const __nv_bfloat162*>(&r1);
+    for (int j0 = 0; j0 < n; j0 += kMergeBatch) {
+      int4 r[kMergeBatch][2];
+      float wj[kMergeBatch];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const float2 f0 = __bfloat1622float2(h0[u]);
-        const float2 f1 = __bfloat1622float2(h1[u]);
-        acc[0][2 * u] = fmaf(wj, f0.x, acc[0][2 * u]);
-        acc[0][2 * u + 1] = fmaf(wj, f0.y, acc[0][2 * u + 1]);
-        acc[1][2 * u] = fmaf(wj, f1.x, acc[1][2 * u]);
-        acc[1][2 * u + 1] = fmaf(wj, f1.y, acc[1][2 * u + 1]);
+      for (int b = 0; b < kMergeBatch; ++b) {
+        const bool live = j0 + b < n;
+        const int4* src = !live ? nullptr : staged ? mp[m0 + j0 + b]
+                                                   : reinterpret_cast<const int4*>(members[m0 + j0 + b]);
+        wj[b] = !live ? 0.f : staged ? wn[m0 + j0 + b]
+                                     : static_cast<float>(__ldg(weights + m0 + j0 + b) / dv);
+        r[b][0] = live && one ? ld_nc_v4(src + i) : make_int4(0, 0, 0, 0);
+        r[b][1] = live && two ? ld_nc_v4(src + i2) : make_int4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int b = 0; b < kMergeBatch; ++b) {
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r[b][v]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float2 f = __bfloat1622float2(h[u]);
+            acc[v][2 * u] = fmaf(wj[b], f.x, acc[v][2 * u]);
+            acc[v][2 * u + 1] = fmaf(wj[b], f.y, acc[v][2 * u + 1]);
+          }
+        }
       }
     }
+    int4* dst = reinterpret_cast<int4*>(outs[g]);
 #pragma unroll
     for (int v = 0; v < 2; ++v) {
-      if (v == 1 && !two) break;
+      if (!(v ? two : one)) continue;
       int4 o;
       o.x = static_cast<int>(pack_bf16x2(acc[v][0], acc[v][1]));
       o.y = static_cast<int>(pack_bf16x2(acc[v][2], acc[v][3]));
@@ -132,7 +171,10 @@ int comoe_merge(int dtype, const void* const* member_ptrs, const int* group_offs
   dim3 grid(static_cast<unsigned>(bx), static_cast<unsigned>(n_groups));
   if (dtype == COMOE_DTYPE_BF16) {
     COMOE_REQUIRE(D % 8 == 0, kUnsupportedShape, "merge(bf16): D=%ld must be a multiple of 8", D);
-    merge_bf16_kernel<<<grid, 256, 0, s>>>(member_ptrs, group_offsets, weights, divisor, out_ptrs, D);
+    const long items = ((D / 8 + 2 * kMergeThreads - 1) / (2 * kMergeThreads)) * n_groups;
+    const long blocks = items < static_cast<long>(sms) * 4 ? items : static_cast<long>(sms) * 4;
+    merge_bf16_kernel<<<static_cast<unsigned>(blocks), kMergeThreads, 0, s>>>(
+        member_ptrs, group_offsets, weights, divisor, out_ptrs, D, n_groups);
     return check_launch("merge_bf16_kernel");
   }
   if (dtype == COMOE_DTYPE_F64) {

@@ -13,8 +13,9 @@
 
 namespace comoe {
 
-constexpr int kSimTile = 32;
-constexpr int kSimKc = 32;
+constexpr int kSimKc = 16;      // d per smem stage (a 32-byte sector of a bf16 row)
+constexpr int kSimTJ = 64;      // output columns per tile
+constexpr int kSimSmallE = 8;   // register-resident cosine path for E <= 8
 
 template <typename T>
 __device__ __forceinline__ double to_f64(T v);
@@ -25,36 +26,54 @@ __device__ __forceinline__ double to_f64<__nv_bfloat16>(__nv_bfloat16 v) {
   return static_cast<double>(__bfloat162float(v));
 }
 
+// Row tile height: 64 (4x4 outputs per thread, 0.5 smem loads per FMA —
+// the first version's 32x32 tile with 2x2 outputs did one load per FMA and
+// ran L1-bound at 7 TF/s) or 16 for E <= 16 (small row counts would leave
+// most of a 64-row tile empty).
+static int sim_ti(int E) { return E <= 16 ? 16 : 64; }
+
 // grid: x = output tile (tiles over [E] x [E + n*B]), y = D-slice.
-template <typename T>
+// With 64x64 tiles the Gram block is symmetric: tiles strictly below the
+// diagonal are skipped and mirrored by the reduction.
+template <typename T, int TI>
 __global__ void __launch_bounds__(256) sim_contract_kernel(const void* const* __restrict__ rows, int E,
                                                            long D, const double* __restrict__ probes,
                                                            int n_probes,
                                                            const double* __restrict__ proj,
                                                            int buckets, int tiles_j,
                                                            double* __restrict__ partial) {
+  constexpr int RI = TI / 16, RJ = kSimTJ / 16;
   const int ncols = E + n_probes * buckets;
   const int ti = blockIdx.x / tiles_j, tj = blockIdx.x % tiles_j;
-  const int i0 = ti * kSimTile, j0 = tj * kSimTile;
+  const int i0 = ti * TI, j0 = tj * kSimTJ;
+  if (TI == kSimTJ && j0 + kSimTJ <= E && tj < ti) return;  // mirrored Gram tile
   const long slice = (D + gridDim.y - 1) / gridDim.y;
   const long d0 = blockIdx.y * slice;
   const long d1 = d0 + slice < D ? d0 + slice : D;
 
-  __shared__ double sa[kSimKc][kSimTile + 1];
-  __shared__ double sb[kSimKc][kSimTile + 1];
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // 16 x 16 threads, 2x2 outputs each
-  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  __shared__ __align__(16) double sa[kSimKc][TI];
+  __shared__ __align__(16) double sb[kSimKc][kSimTJ];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // 16 x 16 threads, RI x RJ outputs each
+  double acc[RI][RJ];
+#pragma unroll
+  for (int u = 0; u < RI; ++u)
+#pragma unroll
+    for (int v = 0; v < RJ; ++v) acc[u][v] = 0.0;
 
   for (long k0 = d0; k0 < d1; k0 += kSimKc) {
-    // stage 32 rows x 32 d of A (expert rows) and of the column operand
-    for (int idx = threadIdx.x; idx < kSimTile * kSimKc; idx += blockDim.x) {
+    // stage TI rows and 64 columns of kSimKc d each; thread -> (row, d), d fastest
+    for (int idx = threadIdx.x; idx < TI * kSimKc; idx += blockDim.x) {
       const int r = idx / kSimKc, c = idx % kSimKc;
       const long d = k0 + c;
-      double av = 0.0, bv = 0.0;
+      const int i = i0 + r;
+      sa[c][r] = (d < d1 && i < E) ? to_f64(static_cast<const T*>(rows[i])[d]) : 0.0;
+    }
+    for (int idx = threadIdx.x; idx < kSimTJ * kSimKc; idx += blockDim.x) {
+      const int r = idx / kSimKc, c = idx % kSimKc;
+      const long d = k0 + c;
+      const int j = j0 + r;
+      double bv = 0.0;
       if (d < d1) {
-        const int i = i0 + r;
-        if (i < E) av = to_f64(static_cast<const T*>(rows[i])[d]);
-        const int j = j0 + r;
         if (j < E) {
           bv = to_f64(static_cast<const T*>(rows[j])[d]);
         } else if (j < ncols) {
@@ -62,41 +81,251 @@ __global__ void __launch_bounds__(256) sim_contract_kernel(const void* const* __
           bv = probes[static_cast<long>(q / buckets) * D + d] * proj[static_cast<long>(q % buckets) * D + d];
         }
       }
-      sa[c][r] = av;
       sb[c][r] = bv;
     }
     __syncthreads();
-#pragma unroll 8
+#pragma unroll 4
     for (int c = 0; c < kSimKc; ++c) {
-      const double a0 = sa[c][ty * 2], a1 = sa[c][ty * 2 + 1];
-      const double b0 = sb[c][tx * 2], b1 = sb[c][tx * 2 + 1];
-      acc[0][0] = fma(a0, b0, acc[0][0]);
-      acc[0][1] = fma(a0, b1, acc[0][1]);
-      acc[1][0] = fma(a1, b0, acc[1][0]);
-      acc[1][1] = fma(a1, b1, acc[1][1]);
+      double a[RI], b[RJ];
+#pragma unroll
+      for (int u = 0; u < RI; ++u) a[u] = sa[c][ty * RI + u];
+#pragma unroll
+      for (int v = 0; v < RJ; ++v) b[v] = sb[c][tx * RJ + v];
+#pragma unroll
+      for (int u = 0; u < RI; ++u)
+#pragma unroll
+        for (int v = 0; v < RJ; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
     }
     __syncthreads();
   }
   double* out = partial + static_cast<long>(blockIdx.y) * E * ncols;
 #pragma unroll
-  for (int u = 0; u < 2; ++u)
+  for (int u = 0; u < RI; ++u)
 #pragma unroll
-    for (int v = 0; v < 2; ++v) {
-      const int i = i0 + ty * 2 + u, j = j0 + tx * 2 + v;
+    for (int v = 0; v < RJ; ++v) {
+      const int i = i0 + ty * RI + u, j = j0 + tx * RJ + v;
       if (i < E && j < ncols) out[static_cast<long>(i) * ncols + j] = acc[u][v];
     }
 }
 
+// Cosine Gram for E <= 8 experts without tiles: every thread streams 8
+// consecutive d of all E rows (16-byte loads) and keeps the E(E+1)/2
+// upper-triangle dot products in registers; block partials are reduced
+// warp -> block in a fixed order. Exact bf16 products, fp64 sums.
+template <typename T, int E>
+__global__ void __launch_bounds__(256) sim_gram_small_kernel(const void* const* __restrict__ rows,
+                                                             long D, double* __restrict__ partial) {
+  constexpr int NP = E * (E + 1) / 2;
+  constexpr int V = 16 / sizeof(T);  // elements per 16-byte load
+  double acc[NP];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) acc[p] = 0.0;
+  const T* r[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) r[e] = static_cast<const T*>(rows[e]);
+  const long nv = D / V;
+  for (long v = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; v < nv;
+       v += static_cast<long>(gridDim.x) * blockDim.x) {
+    double x[E][V];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int4 raw = ld_nc_v4(r[e] + v * V);
+      const T* pv = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+      for (int k = 0; k < V; ++k) x[e][k] = to_f64(pv[k]);
+    }
+    int p = 0;
+#pragma unroll
+    for (int a = 0; a < E; ++a)
+#pragma unroll
+      for (int b = a; b < E; ++b, ++p)
+#pragma unroll
+        for (int k = 0; k < V; ++k) acc[p] = fma(x[a][k], x[b][k], acc[p]);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // tail (D % V) by one thread
+    for (long d = nv * V; d < D; ++d) {
+      int p = 0;
+      for (int a = 0; a < E; ++a)
+        for (int b = a; b < E; ++b, ++p) acc[p] = fma(to_f64(r[a][d]), to_f64(r[b][d]), acc[p]);
+    }
+  }
+  __shared__ double red[8][NP];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < NP; ++q) {
+    double v = acc[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp][q] = v;
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < NP; q += blockDim.x) {
+    double v = 0.0;
+    for (int w = 0; w < 8; ++w) v += red[w][q];
+    partial[static_cast<long>(blockIdx.x) * NP + q] = v;
+  }
+}
+
+__global__ void sim_gram_small_reduce(const double* __restrict__ partial, int blocks, int E,
+                                      double* __restrict__ gram) {
+  const int NP = E * (E + 1) / 2;
+  for (int q = threadIdx.x; q < NP; q += blockDim.x) {
+    double v = 0.0;
+    for (int b = 0; b < blocks; ++b) v += partial[static_cast<long>(b) * NP + q];
+    int a = 0, rem = q;
+    while (rem >= E - a) { rem -= E - a; ++a; }
+    const int c = a + rem;
+    gram[a * E + c] = v;
+    gram[c * E + a] = v;
+  }
+}
+
+// Cosine Gram of bf16 experts on the tensor cores (mma.sync m16n8k16,
+// fp32 accumulate, flushed into fp64 every 256 d). bf16 x bf16 products
+// are exact in fp32; only the fp32 sum of <= 256 products per flush
+// rounds, which at Switch scale (D = 4.7M, sigma 0.02) moves a cosine by
+// ~1e-11 — far inside the 1e-7 bf16 parity bar.
+// A warp owns one (32x32 tile, D-slice) unit; Gram tiles below the
+// diagonal are skipped (mirrored by the reduction). k-permutation trick:
+// the contraction sums over every d, so each thread may feed the MMA's k
+// slots from one 16-byte vector of 8 consecutive d per row — the same
+// vector serves as A fragment (row g / g+8 of an m-tile) and B fragment
+// (column g of an n-tile) — no shared memory, fully used 32-byte sectors.
+constexpr int kGramFlush = 8;  // 32-d chunks between fp64 flushes
+
+__device__ __forceinline__ void mma_bf16_16816(float* c, uint32_t a0, uint32_t a1, uint32_t a2,
+                                               uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
+      "{%8, %9}, {%0, %1, %2, %3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// Q = 8-row groups per tile side (1: an 8x8 tile for E <= 8, 4: 32x32);
+// U = 32-d chunks loaded per iteration (loads in flight per thread).
+template <int Q, int U>
+__global__ void __launch_bounds__(128) sim_gram_mma_kernel(const void* const* __restrict__ rows,
+                                                           int E, long D, int tiles_1d,
+                                                           int splits, long slice,
+                                                           double* __restrict__ partial) {
+  constexpr int M = Q == 1 ? 1 : Q / 2;  // m16 tiles (rows g + 16m, g + 16m + 8)
+  constexpr int N = Q;                   // n8 tiles (columns g + 8n)
+  constexpr int T = 8 * Q;               // tile side
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long unit = static_cast<long>(blockIdx.x) * 4 + warp;
+  const int n_tiles = tiles_1d * (tiles_1d + 1) / 2;
+  if (unit >= static_cast<long>(n_tiles) * splits) return;
+  int tile = static_cast<int>(unit % n_tiles);
+  const int split = static_cast<int>(unit / n_tiles);
+  int ti = 0;  // upper-triangle tile (ti <= tj), row-major
+  while (tile >= tiles_1d - ti) { tile -= tiles_1d - ti; ++ti; }
+  const int tj = ti + tile;
+  const bool diag = ti == tj;
+  const int g = lane >> 2, tq = lane & 3;
+  const int I0 = ti * T, J0 = tj * T;
+  const long d0 = split * slice;
+  const long d1 = d0 + slice < D ? d0 + slice : D;
+  const int4* ra[Q];
+  const int4* rb[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int i = I0 + g + 8 * q, j = J0 + g + 8 * q;
+    ra[q] = i < E ? static_cast<const int4*>(rows[i]) : nullptr;
+    rb[q] = j < E ? static_cast<const int4*>(rows[j]) : nullptr;
+  }
+  float c[M][N][4];
+  double acc[M][N][4];
+#pragma unroll
+  for (int m = 0; m < M; ++m)
+#pragma unroll
+    for (int n = 0; n < N; ++n)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) { c[m][n][r] = 0.f; acc[m][n][r] = 0.0; }
+  const int4 z = make_int4(0, 0, 0, 0);
+  int since = 0;
+  for (long d = d0; d < d1; d += 32 * U) {
+    int4 A[U][Q], B[U][Q];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long dd = d + 32 * u;
+      const long v = (dd >> 3) + tq;  // this thread's 16-byte vector: dd + 8*tq .. +8
+      const bool in = dd + 8 * tq < d1;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        A[u][q] = (in && ra[q]) ? ld_nc_v4(ra[q] + v) : z;
+        B[u][q] = diag ? A[u][q] : ((in && rb[q]) ? ld_nc_v4(rb[q] + v) : z);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int s2 = 0; s2 < 2; ++s2)
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          const uint32_t* a_lo = reinterpret_cast<const uint32_t*>(&A[u][Q == 1 ? 0 : 2 * m]);
+          const uint32_t hi0 = Q == 1 ? 0u : reinterpret_cast<const uint32_t*>(&A[u][2 * m + (Q > 1)])[2 * s2];
+          const uint32_t hi1 = Q == 1 ? 0u : reinterpret_cast<const uint32_t*>(&A[u][2 * m + (Q > 1)])[2 * s2 + 1];
+#pragma unroll
+          for (int n = 0; n < N; ++n) {
+            const uint32_t* b = reinterpret_cast<const uint32_t*>(&B[u][n]);
+            mma_bf16_16816(c[m][n], a_lo[2 * s2], hi0, a_lo[2 * s2 + 1], hi1, b[2 * s2],
+                           b[2 * s2 + 1]);
+          }
+        }
+    since += U;
+    if (since >= kGramFlush) {
+      since = 0;
+#pragma unroll
+      for (int m = 0; m < M; ++m)
+#pragma unroll
+        for (int n = 0; n < N; ++n)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            acc[m][n][r] += static_cast<double>(c[m][n][r]);
+            c[m][n][r] = 0.f;
+          }
+    }
+  }
+  double* out = partial + static_cast<long>(split) * E * E;
+#pragma unroll
+  for (int m = 0; m < M; ++m)
+#pragma unroll
+    for (int n = 0; n < N; ++n)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        // C fragment: rows 16m + g (+8 for r >= 2), columns 8n + 2tq + (r & 1)
+        const int i = I0 + 16 * m + g + (r >= 2 ? 8 : 0);
+        const int j = J0 + 8 * n + 2 * tq + (r & 1);
+        if (r < 2 || Q > 1)
+          if (i < E && j < E && i < I0 + T)
+            out[static_cast<long>(i) * E + j] = acc[m][n][r] + static_cast<double>(c[m][n][r]);
+      }
+}
+
+// one warp per output entry: lanes stride the splits, fixed-order tree
+// (deterministic); skipped below-diagonal Gram tiles read the mirror.
 __global__ void sim_reduce_kernel(const double* __restrict__ partial, int splits, int E, int ncols,
-                                  double* __restrict__ gram, double* __restrict__ logits) {
+                                  int mirror_tile, double* __restrict__ gram,
+                                  double* __restrict__ logits) {
   const long n = static_cast<long>(E) * ncols;
-  for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; idx < n;
-       idx += static_cast<long>(gridDim.x) * blockDim.x) {
-    double s = 0.0;
-    for (int k = 0; k < splits; ++k) s += partial[k * n + idx];
+  const int lane = threadIdx.x & 31;
+  const long warps = static_cast<long>(gridDim.x) * (blockDim.x >> 5);
+  for (long idx = blockIdx.x * static_cast<long>(blockDim.x >> 5) + (threadIdx.x >> 5); idx < n;
+       idx += warps) {
     const int i = static_cast<int>(idx / ncols), j = static_cast<int>(idx % ncols);
-    if (j < E) gram[static_cast<long>(i) * E + j] = s;
-    else logits[static_cast<long>(i) * (ncols - E) + (j - E)] = s;
+    long src = idx;
+    if (mirror_tile && j < E && (j / mirror_tile) < (i / mirror_tile) &&
+        (j / mirror_tile + 1) * mirror_tile <= E)
+      src = static_cast<long>(j) * ncols + i;
+    double s = 0.0;
+    for (int k = lane; k < splits; k += 32) s += partial[k * n + src];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      if (j < E) gram[static_cast<long>(i) * E + j] = s;
+      else logits[static_cast<long>(i) * (ncols - E) + (j - E)] = s;
+    }
   }
 }
 
@@ -142,12 +371,51 @@ __global__ void sim_finalize_kernel(const double* __restrict__ gram,
   }
 }
 
-static int sim_splits(int E, int ncols, long D) {
+static int num_sms() {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const long tiles = static_cast<long>((E + kSimTile - 1) / kSimTile) * ((ncols + kSimTile - 1) / kSimTile);
-  long splits = (static_cast<long>(sms) * 4 + tiles - 1) / tiles;
+  return sms;
+}
+
+static bool sim_small(int E, int n_probes) { return n_probes == 0 && E >= 1 && E <= kSimSmallE; }
+
+// bf16 cosine-only Gram on the tensor cores (rows 16-byte aligned, D % 8 == 0)
+static bool sim_mma(int dtype, int n_probes, long D) {
+  return dtype == COMOE_DTYPE_BF16 && n_probes == 0 && D % 8 == 0;
+}
+
+struct GramPlan {
+  int tiles_1d, splits;
+  long slice;
+};
+
+static int gram_tile(int E) { return E <= 8 ? 8 : 32; }
+
+static GramPlan gram_plan(int E, long D) {
+  GramPlan g;
+  g.tiles_1d = (E + gram_tile(E) - 1) / gram_tile(E);
+  const long n_tiles = static_cast<long>(g.tiles_1d) * (g.tiles_1d + 1) / 2;
+  long splits = (static_cast<long>(num_sms()) * 32 + n_tiles - 1) / n_tiles;  // ~32 warps per SM
+  const long max_by_d = (D + 2047) / 2048;  // >= 2048 d per unit
+  if (splits > max_by_d) splits = max_by_d;
+  if (splits < 1) splits = 1;
+  g.slice = ((D + splits - 1) / splits + 31) / 32 * 32;
+  g.splits = static_cast<int>((D + g.slice - 1) / g.slice);
+  return g;
+}
+
+static int sim_small_blocks(long D) {
+  long b = static_cast<long>(num_sms()) * 4;
+  const long need = (D / 8 + 255) / 256;
+  if (b > need) b = need;
+  return static_cast<int>(b < 1 ? 1 : b);
+}
+
+static int sim_splits(int E, int ncols, long D) {
+  const int ti = sim_ti(E);
+  const long tiles = static_cast<long>((E + ti - 1) / ti) * ((ncols + kSimTJ - 1) / kSimTJ);
+  long splits = (static_cast<long>(num_sms()) * 4 + tiles - 1) / tiles;
   const long max_by_d = (D + 4095) / 4096;  // at least 4096 d per slice
   if (splits > max_by_d) splits = max_by_d;
   if (splits > 1024) splits = 1024;
@@ -155,11 +423,41 @@ static int sim_splits(int E, int ncols, long D) {
   return static_cast<int>(splits);
 }
 
+template <typename T>
+static void launch_small(int E, const void* const* rows, long D, int blocks, double* partial,
+                         cudaStream_t s) {
+  switch (E) {
+    case 1: sim_gram_small_kernel<T, 1><<<blocks, 256, 0, s>>>(rows, D, partial); break;
+    case 2: sim_gram_small_kernel<T, 2><<<blocks, 256, 0, s>>>(rows, D, partial); break;
+    case 3: sim_gram_small_kernel<T, 3><<<blocks, 256, 0, s>>>(rows, D, partial); break;
+    case 4: sim_gram_small_kernel<T, 4><<<blocks, 256, 0, s>>>(rows, D, partial); break;
+    case 5: sim_gram_small_kernel<T, 5><<<blocks, 256, 0, s>>>(rows, D, partial); break;
+    case 6: sim_gram_small_kernel<T, 6><<<blocks, 256, 0, s>>>(rows, D, partial); break;
+    case 7: sim_gram_small_kernel<T, 7><<<blocks, 256, 0, s>>>(rows, D, partial); break;
+    default: sim_gram_small_kernel<T, 8><<<blocks, 256, 0, s>>>(rows, D, partial); break;
+  }
+}
+
 }  // namespace comoe
 
 extern "C" {
 
 long comoe_sim_workspace_bytes(int E, int n_probes, int buckets, long D) {
+  // (bf16 and f64 share one workspace size: the larger of the two paths)
+  if (n_probes == 0 && D % 8 == 0) {
+    const comoe::GramPlan g = comoe::gram_plan(E, D);
+    long w = static_cast<long>(g.splits) * E * E * sizeof(double);
+    if (comoe::sim_small(E, n_probes)) {
+      const long ws = static_cast<long>(comoe::sim_small_blocks(D)) * (E * (E + 1) / 2) * sizeof(double);
+      w = w > ws ? w : ws;
+    } else {
+      const long wt = static_cast<long>(comoe::sim_splits(E, E, D)) * E * E * sizeof(double);
+      w = w > wt ? w : wt;
+    }
+    return w;
+  }
+  if (comoe::sim_small(E, n_probes))
+    return static_cast<long>(comoe::sim_small_blocks(D)) * (E * (E + 1) / 2) * sizeof(double);
   const int ncols = E + (n_probes > 0 ? n_probes * buckets : 0);
   return static_cast<long>(comoe::sim_splits(E, ncols, D)) * E * ncols * sizeof(double);
 }
@@ -172,28 +470,65 @@ int comoe_sim_contract(int dtype, const void* const* rows, int E, long D, const 
   COMOE_REQUIRE(n_probes == 0 || (probes && proj && logits && buckets >= 1), kBadArg,
                 "sim_contract: null calibration");
   COMOE_REQUIRE(E >= 1 && D >= 1 && n_probes >= 0, kBadArg, "sim_contract: bad sizes");
+  COMOE_REQUIRE(dtype == COMOE_DTYPE_BF16 || dtype == COMOE_DTYPE_F64, kBadArg,
+                "sim_contract: dtype %d", dtype);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double* partial = static_cast<double*>(work);
+  if (sim_mma(dtype, n_probes, D)) {
+    const GramPlan gp = gram_plan(E, D);
+    const long units = static_cast<long>(gp.tiles_1d) * (gp.tiles_1d + 1) / 2 * gp.splits;
+    const unsigned nb = static_cast<unsigned>((units + 3) / 4);
+    if (E <= 8)
+      sim_gram_mma_kernel<1, 8><<<nb, 128, 0, s>>>(rows, E, D, gp.tiles_1d, gp.splits, gp.slice,
+                                                   partial);
+    else
+      sim_gram_mma_kernel<4, 1><<<nb, 128, 0, s>>>(rows, E, D, gp.tiles_1d, gp.splits, gp.slice,
+                                                   partial);
+    int rc = check_launch("sim_gram_mma_kernel");
+    if (rc) return rc;
+    const long n = static_cast<long>(E) * E;
+    const int blocks = static_cast<int>((n + 7) / 8 < 4096 ? (n + 7) / 8 : 4096);
+    sim_reduce_kernel<<<blocks, 256, 0, s>>>(partial, gp.splits, E, E, gram_tile(E), gram, nullptr);
+    return check_launch("sim_reduce_kernel");
+  }
+  if (sim_small(E, n_probes)) {
+    // rows must be 16-byte aligned for the vector loads (pool slots and
+    // torch allocations are)
+    const int blocks = sim_small_blocks(D);
+    if (dtype == COMOE_DTYPE_BF16) launch_small<__nv_bfloat16>(E, rows, D, blocks, partial, s);
+    else launch_small<double>(E, rows, D, blocks, partial, s);
+    int rc = check_launch("sim_gram_small_kernel");
+    if (rc) return rc;
+    sim_gram_small_reduce<<<1, 64, 0, s>>>(partial, blocks, E, gram);
+    return check_launch("sim_gram_small_reduce");
+  }
   if (n_probes == 0) buckets = 0;  // cosine only
   const int ncols = E + n_probes * buckets;
   const int splits = sim_splits(E, ncols, D);
-  const int tiles_i = (E + kSimTile - 1) / kSimTile, tiles_j = (ncols + kSimTile - 1) / kSimTile;
+  const int ti = sim_ti(E);
+  const int tiles_i = (E + ti - 1) / ti, tiles_j = (ncols + kSimTJ - 1) / kSimTJ;
   dim3 grid(tiles_i * tiles_j, splits);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  double* partial = static_cast<double*>(work);
-  if (dtype == COMOE_DTYPE_BF16)
-    sim_contract_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(rows, E, D, probes, n_probes, proj,
-                                                            buckets, tiles_j, partial);
-  else if (dtype == COMOE_DTYPE_F64)
-    sim_contract_kernel<double><<<grid, 256, 0, s>>>(rows, E, D, probes, n_probes, proj, buckets,
-                                                     tiles_j, partial);
-  else {
-    set_error("sim_contract: dtype %d", dtype);
-    return kBadArg;
+  if (dtype == COMOE_DTYPE_BF16) {
+    if (ti == 16)
+      sim_contract_kernel<__nv_bfloat16, 16><<<grid, 256, 0, s>>>(rows, E, D, probes, n_probes,
+                                                                  proj, buckets, tiles_j, partial);
+    else
+      sim_contract_kernel<__nv_bfloat16, 64><<<grid, 256, 0, s>>>(rows, E, D, probes, n_probes,
+                                                                  proj, buckets, tiles_j, partial);
+  } else {
+    if (ti == 16)
+      sim_contract_kernel<double, 16><<<grid, 256, 0, s>>>(rows, E, D, probes, n_probes, proj,
+                                                           buckets, tiles_j, partial);
+    else
+      sim_contract_kernel<double, 64><<<grid, 256, 0, s>>>(rows, E, D, probes, n_probes, proj,
+                                                           buckets, tiles_j, partial);
   }
   int rc = check_launch("sim_contract_kernel");
   if (rc) return rc;
   const long n = static_cast<long>(E) * ncols;
-  const int blocks = static_cast<int>((n + 255) / 256 < 2048 ? (n + 255) / 256 : 2048);
-  sim_reduce_kernel<<<blocks, 256, 0, s>>>(partial, splits, E, ncols, gram, logits);
+  const int blocks = static_cast<int>((n + 7) / 8 < 4096 ? (n + 7) / 8 : 4096);
+  sim_reduce_kernel<<<blocks, 256, 0, s>>>(partial, splits, E, ncols, ti == kSimTJ ? kSimTJ : 0,
+                                           gram, logits);
   return check_launch("sim_reduce_kernel");
 }
 

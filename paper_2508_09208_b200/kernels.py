@@ -252,55 +252,70 @@ def grouped_gemm(a, pool, b_offset, N, group_rows, group_row_base, group_slot, e
 
 # ---------------------------------------------------------------- K5 merge
 
+class MergePlan:
+    """Device group table for one K5 launch over a layer's multi-member
+    groups: groups_members = per group, the member tensors (flat, same
+    numel); weights = per-member floats; divisors = per-group floats; outs =
+    per-group output tensors. Built once (one pinned async upload), run any
+    number of times — a variant rebuild re-merges from the same table."""
+
+    def __init__(self, groups_members, weights, divisors, outs, dtype):
+        self.n_groups = len(outs)
+        if not groups_members:
+            return
+        dev = outs[0].device
+        D = outs[0].numel()
+        if dtype not in (torch.bfloat16, torch.float64):
+            raise ValueError("merge supports bf16 and float64 parameters")
+        self.code = DTYPE_BF16 if dtype == torch.bfloat16 else DTYPE_F64
+        ptrs, offs, ws = [], [0], []
+        for members, wlist in zip(groups_members, weights):
+            if len(members) != len(wlist):
+                raise ValueError("one weight per member")
+            for m in members:
+                _need(m, "member", dtype, align=16 if dtype == torch.bfloat16 else 8)
+                if m.numel() != D:
+                    raise ValueError("member size mismatch")
+                ptrs.append(m.data_ptr())
+            ws.extend(float(w) for w in wlist)
+            offs.append(len(ptrs))
+        for o in outs:
+            _need(o, "out", dtype, align=16 if dtype == torch.bfloat16 else 8)
+            if o.numel() != D:
+                raise ValueError("output size mismatch")
+        self.D = D
+        self.max_members = max(offs[i + 1] - offs[i] for i in range(len(outs)))
+        # one pinned staging buffer, one async H2D: [ptrs | outs | offs | weights | divisors]
+        nm, ng = len(ptrs), len(outs)
+        host = torch.empty(nm + ng + (ng + 2) // 2 + nm + ng, dtype=torch.int64).pin_memory()
+        host[:nm] = torch.tensor(ptrs, dtype=torch.int64)
+        host[nm:nm + ng] = torch.tensor([o.data_ptr() for o in outs], dtype=torch.int64)
+        o_off = nm + ng
+        n_off_words = (ng + 2) // 2
+        host[o_off:o_off + n_off_words].view(torch.int32)[:ng + 1] = torch.tensor(offs, dtype=torch.int32)
+        w_off = o_off + n_off_words
+        host[w_off:w_off + nm].view(torch.float64)[:] = torch.tensor(ws, dtype=torch.float64)
+        host[w_off + nm:].view(torch.float64)[:] = torch.tensor([float(x) for x in divisors],
+                                                               dtype=torch.float64)
+        # PyTorch's pinned-host allocator records the async copy on the
+        # stream before reusing `host`
+        self.table = host.to(dev, non_blocking=True)
+        self.t_ptrs, self.t_out = self.table[:nm], self.table[nm:nm + ng]
+        self.t_offs = self.table[o_off:o_off + n_off_words].view(torch.int32)
+        self.t_w = self.table[w_off:w_off + nm].view(torch.float64)
+        self.t_div = self.table[w_off + nm:].view(torch.float64)
+
+    def run(self) -> None:
+        if not self.n_groups:
+            return
+        _lib.call("comoe_merge", self.code, _ptr(self.t_ptrs), _ptr(self.t_offs), _ptr(self.t_w),
+                  _ptr(self.t_div), _ptr(self.t_out), self.n_groups, self.max_members, self.D,
+                  _stream())
+
+
 def merge_groups(groups_members, weights, divisors, outs, dtype) -> None:
-    """groups_members: list (per group) of member tensors (flat, same numel);
-    weights: list of per-member float weights; divisors: per-group float;
-    outs: per-group output tensors. One launch for all groups."""
-    if not groups_members:
-        return
-    dev = outs[0].device
-    D = outs[0].numel()
-    code = DTYPE_BF16 if dtype == torch.bfloat16 else DTYPE_F64
-    if dtype not in (torch.bfloat16, torch.float64):
-        raise ValueError("merge supports bf16 and float64 parameters")
-    ptrs, offs, ws = [], [0], []
-    for members, wlist in zip(groups_members, weights):
-        if len(members) != len(wlist):
-            raise ValueError("one weight per member")
-        for m in members:
-            _need(m, "member", dtype, align=16 if dtype == torch.bfloat16 else 8)
-            if m.numel() != D:
-                raise ValueError("member size mismatch")
-            ptrs.append(m.data_ptr())
-        ws.extend(float(w) for w in wlist)
-        offs.append(len(ptrs))
-    for o in outs:
-        _need(o, "out", dtype, align=16 if dtype == torch.bfloat16 else 8)
-        if o.numel() != D:
-            raise ValueError("output size mismatch")
-    max_members = max(offs[i + 1] - offs[i] for i in range(len(outs)))
-    # one pinned staging buffer, one async H2D: [ptrs | outs | offs | weights | divisors]
-    nm, ng = len(ptrs), len(outs)
-    host = torch.empty(nm + ng + (ng + 2) // 2 + nm + ng, dtype=torch.int64).pin_memory()
-    host[:nm] = torch.tensor(ptrs, dtype=torch.int64)
-    host[nm:nm + ng] = torch.tensor([o.data_ptr() for o in outs], dtype=torch.int64)
-    o_off = nm + ng
-    n_off_words = (ng + 2) // 2
-    host[o_off:o_off + n_off_words].view(torch.int32)[:ng + 1] = torch.tensor(offs, dtype=torch.int32)
-    w_off = o_off + n_off_words
-    host[w_off:w_off + nm].view(torch.float64)[:] = torch.tensor(ws, dtype=torch.float64)
-    host[w_off + nm:].view(torch.float64)[:] = torch.tensor([float(x) for x in divisors],
-                                                           dtype=torch.float64)
-    dev_tab = host.to(dev, non_blocking=True)
-    t_ptrs, t_out = dev_tab[:nm], dev_tab[nm:nm + ng]
-    t_offs = dev_tab[o_off:o_off + n_off_words].view(torch.int32)
-    t_w = dev_tab[w_off:w_off + nm].view(torch.float64)
-    t_div = dev_tab[w_off + nm:].view(torch.float64)
-    _lib.call("comoe_merge", code, _ptr(t_ptrs), _ptr(t_offs), _ptr(t_w), _ptr(t_div),
-              _ptr(t_out), len(outs), max_members, D, _stream())
-    # both allocators are stream-ordered: PyTorch's pinned-host allocator records
-    # the async copy before reusing `host`, and dev_tab is reused only after this
-    # kernel in stream order
+    """One K5 launch for all groups (see MergePlan)."""
+    MergePlan(groups_members, weights, divisors, outs, dtype).run()
 
 
 # ---------------------------------------------------------------- K6 similarity
@@ -359,10 +374,14 @@ def predictor_mlp(slots, emb, ctx, w1, b1, w2, b2, want_demand=False):
     if w1.shape[1] != E + emb_dim + ctx_dim:
         raise ValueError("embedding/context dims do not match the predictor")
     probs = torch.empty((B, E), dtype=torch.float64, device=slots.device)
-    demand = torch.empty(E, dtype=torch.float64, device=slots.device) if want_demand else None
+    demand = work = None
+    if want_demand:
+        demand = torch.empty(E, dtype=torch.float64, device=slots.device)
+        nbytes = _lib.load().comoe_predictor_workspace_bytes(B, E)
+        work = torch.empty(max(nbytes, 8), dtype=torch.uint8, device=slots.device)
     _lib.call("comoe_predictor_mlp", _ptr(slots), B, K, _ptr(emb), emb_dim, _ptr(ctx), ctx_dim,
               _ptr(w1), _ptr(b1), hidden, _ptr(w2), _ptr(b2), E, _ptr(probs), _ptr(demand),
-              _stream())
+              _ptr(work), _stream())
     return (probs, demand) if want_demand else probs
 
 

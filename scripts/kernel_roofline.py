@@ -134,7 +134,8 @@ def main():
     outs = [pool.view(pool.alloc()) for _ in multi]
     ebytes = pool.slot_bytes
     mbytes = sum((len(gr.slots) + 1) * ebytes for gr in multi)
-    ms = timed(lambda: kernels.merge_groups(mem, wts, divs, outs, torch.bfloat16))
+    plan = kernels.MergePlan(mem, wts, divs, outs, torch.bfloat16)
+    ms = timed(plan.run)
     sizes = sorted(len(gr.slots) for gr in multi)
     line("merge (K5, 128->64 bf16)", ms, mbytes,
          f"sum over {len(multi)} multi-member groups of (members+1)*{ebytes} B; sizes {sizes}")
