@@ -1,6 +1,7 @@
 // C-ABI plumbing: error reporting, tensor-map encoding, version.
 #include <cudaTypedefs.h>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <mutex>
 
@@ -16,6 +17,17 @@ void set_error(const char* fmt, ...) {
   va_start(ap, fmt);
   vsnprintf(g_err, sizeof(g_err), fmt, ap);
   va_end(ap);
+}
+
+int pdl_attr(cudaLaunchAttribute* attr) {
+  static const bool on = [] {
+    const char* e = std::getenv("COMOE_PDL");
+    return e && e[0] == '1';
+  }();
+  if (!on) return 0;
+  attr->id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr->val.programmaticStreamSerializationAllowed = 1;
+  return 1;
 }
 
 int check_launch(const char* what) {

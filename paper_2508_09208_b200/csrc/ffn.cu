@@ -60,7 +60,15 @@ static int launch_gemm_2sm_cfg(const CUtensorMap& tw, const CUtensorMap& tx,
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  kern<<<sms & ~1, C::kThreads, C::kTotal, stream>>>(tw, tx, to, p);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(sms & ~1);
+  cfg.blockDim = dim3(C::kThreads);
+  cfg.dynamicSmemBytes = C::kTotal;
+  cfg.stream = stream;
+  cudaLaunchAttribute attrs[1];  // (cluster shape comes from __cluster_dims__)
+  cfg.attrs = attrs;
+  cfg.numAttrs = pdl_attr(&attrs[0]);
+  cudaLaunchKernelEx(&cfg, kern, tw, tx, to, p);
   return check_launch("grouped_gemm_2sm_kernel");
 }
 

@@ -130,6 +130,8 @@ __global__ void __launch_bounds__(kGateThreads, 1)
       tmem_alloc<kTmemCols>(tmem_slot);
     }
   }
+  pdl_wait();     // x / slot_map may come from the preceding kernel
+  pdl_trigger();  // persistent grid: the next kernel may launch and wait
   for (int e = threadIdx.x; e < kGateMaxE; e += blockDim.x)
     smap[e] = e < p.E ? (p.slot_map ? __ldg(p.slot_map + e) : e) : -1;
   tc_fence_before();
@@ -382,18 +384,26 @@ static int launch_gate(const CUtensorMap& tx, const CUtensorMap& tw, const GateP
     cfg.blockDim = dim3(kGateThreads);
     cfg.dynamicSmemBytes = S::kTotal;
     cfg.stream = stream;
-    cudaLaunchAttribute attrs[1];
+    cudaLaunchAttribute attrs[2];
     attrs[0].id = cudaLaunchAttributeClusterDimension;
     attrs[0].val.clusterDim.x = 2;
     attrs[0].val.clusterDim.y = 1;
     attrs[0].val.clusterDim.z = 1;
     cfg.attrs = attrs;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 1 + pdl_attr(&attrs[1]);
     cudaLaunchKernelEx(&cfg, kern, tx, tw, p);
     return check_launch("gate_kernel(pair)");
   } else {
     const int grid = p.ntiles < sms ? p.ntiles : sms;
-    kern<<<grid, kGateThreads, S::kTotal, stream>>>(tx, tw, p);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kGateThreads);
+    cfg.dynamicSmemBytes = S::kTotal;
+    cfg.stream = stream;
+    cudaLaunchAttribute attrs[1];
+    cfg.attrs = attrs;
+    cfg.numAttrs = pdl_attr(&attrs[0]);
+    cudaLaunchKernelEx(&cfg, kern, tx, tw, p);
     return check_launch("gate_kernel");
   }
 }
@@ -485,6 +495,7 @@ __global__ void __launch_bounds__(256) route_scan_coop(const int* __restrict__ h
     kept[g] = min(carry, capacity);
     base[g] = sum;
   }
+  pdl_trigger();
 }
 
 // kept = min(count, C); base = exclusive scan of kept.

@@ -39,7 +39,8 @@ struct GroupedGemmParams {
   const int* gather_rows; // 2-SM kernel: B-operand row r of group g is row
                           // gather_rows[row_base[g] + r] of the token tensor (TMA gather4)
   int debug;              // dev-only attribution switches (COMOE_GEMM_DEBUG): 1 = no epilogue
-                          // math/stores, 2 = no TMA (MMA on stale smem); 0 in production
+                          // math/stores, 2 = no TMA (MMA on stale smem), 4 = no TMA store,
+                          // 16/128 = L2-resident operands (see the producer); 0 in production
   int* sched;             // 2-SM kernel: {next tile, finished clusters} counters for dynamic
                           // tile claiming (zero on entry, reset to zero by the last cluster);
                           // nullptr = static round-robin

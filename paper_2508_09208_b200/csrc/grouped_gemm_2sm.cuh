@@ -242,10 +242,10 @@ __device__ __forceinline__ Tile2 decode_tile2(const int* prefix, const GroupedGe
   Tile2 t;
   t.g = find_group(prefix, p.G, tile);
   const int local = tile - prefix[t.g];
+  const int rows = __ldg(p.group_rows + t.g);
   const int tt = local / f_tiles;
   t.ft = local % f_tiles;
   t.tok0 = tt * kTokTile;
-  const int rows = __ldg(p.group_rows + t.g);
   const int n = min(kTokTile, rows - t.tok0);
   t.ntok[0] = min(k2BN, n);
   t.ntok[1] = n - t.ntok[0];
@@ -314,6 +314,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
   }
+  pdl_wait();     // group tables / token rows come from the preceding kernels
+  pdl_trigger();  // persistent grid: the next kernel may launch and wait
   build_tile_prefix_2sm<kTT>(p.group_rows, p.G, f_tiles, prefix);
   tc_fence_before();
   cluster_sync_all();
@@ -359,9 +361,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k
       }
       if (tile >= total_tiles) break;
       const Tile2 t = decode_tile2<kTT>(prefix, p, f_tiles, tile);
-      const int slot = __ldg(p.group_slot + t.g);
+      // (dev attribution: debug 16 = every tile loads slot 0 and token row 0,
+      // 128 = slot 0 only — L2-resident operands; +27-42% / +17% at C2)
+      const int slot = (p.debug & (16 | 128)) ? 0 : __ldg(p.group_slot + t.g);
       const int feat = t.ft * k2BM + static_cast<int>(rank) * 128;
-      const int gbase = __ldg(p.group_row_base + t.g);
+      const int gbase = (p.debug & 16) ? -t.tok0 : __ldg(p.group_row_base + t.g);
       // this CTA's token rows of MMA j: the rank-th half of its nmma[j] columns
       const int row0 = gbase + t.tok0 + static_cast<int>(rank) * (t.nmma[0] >> 1);
       const int row1 = gbase + t.tok0 + k2BN + static_cast<int>(rank) * (t.nmma[1] >> 1);

@@ -35,6 +35,7 @@ constexpr int kTokPerWarp = 4;
 // base is a chain of dependent loads), so row traffic overlaps the index
 // work; then each 32*kRowUnroll-vector slice is stored and the next loaded.
 __global__ void __launch_bounds__(256, 3) permute_kernel(PermuteParams p) {
+  pdl_wait();  // routing tables come from the gate / scan kernels
   const int warps = (gridDim.x * blockDim.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int vec = p.d >> 3;  // uint4 per row
@@ -190,8 +191,14 @@ int comoe_permute(const void* x, int T, int d, int top_k, const int* group_idx,
                   (T + 127) / 128, group_idx, gate_prob, local_rank, tile_offset, group_base,
                   reinterpret_cast<__nv_bfloat16*>(x_perm), row_token, row_prob, token_pos,
                   reinterpret_cast<__nv_bfloat16*>(y_zero)};
-  permute_kernel<<<grid_for_warps((T + kTokPerWarp - 1) / kTokPerWarp), 256, 0,
-                   static_cast<cudaStream_t>(stream)>>>(p);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid_for_warps((T + kTokPerWarp - 1) / kTokPerWarp));
+  cfg.blockDim = dim3(256);
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attrs[1];
+  cfg.attrs = attrs;
+  cfg.numAttrs = pdl_attr(&attrs[0]);
+  cudaLaunchKernelEx(&cfg, permute_kernel, p);
   return check_launch("permute_kernel");
 }
 
