@@ -138,3 +138,85 @@ def test_predictor_matches_numpy():
                                           want_demand=True)
     np.testing.assert_allclose(probs.cpu().numpy(), ref, rtol=1e-10, atol=1e-13)
     np.testing.assert_allclose(demand.cpu().numpy(), ref.sum(0), rtol=1e-10)
+
+
+@pytest.mark.parametrize("E", [3, 8, 13, 40, 128])
+def test_similarity_cosine_tensor_core_paths(E):
+    """bf16 cosine-only Gram (K6 tensor-core path: 8x8 tile for E <= 8,
+    upper-triangle 32x32 tiles with mirroring above) vs fp64 of the same
+    bf16 values, at a D that is not a multiple of the 32-d chunk."""
+    from paper_2508_09208_b200 import kernels
+    D = 100_000 + 8 * 3
+    g = torch.Generator(device="cuda").manual_seed(E)
+    base = torch.randn(4, D, device="cuda", generator=g) * 0.02
+    V = (torch.randn(E, D, device="cuda", generator=g) * 0.02 + base[torch.arange(E) % 4])
+    V = V.to(torch.bfloat16)
+    sim, gram, _ = kernels.similarity([V[e] for e in range(E)], None, None, 1.0)
+    ref = M.cosine_matrix(V.double().cpu().numpy())
+    np.testing.assert_allclose(sim.cpu().numpy(), ref, rtol=1e-7, atol=1e-7)
+    Vh = V.double().cpu().numpy()
+    G = Vh @ Vh.T  # fp32 partial sums: absolute error ~1e-10 of the Gram scale
+    np.testing.assert_allclose(gram.cpu().numpy(), G, rtol=1e-6, atol=1e-9 * np.abs(G).max())
+
+
+@pytest.mark.parametrize("E", [2, 20])
+def test_similarity_f64_and_probe_paths(E):
+    """fp64 parameters (SIMT register path for E <= 8, tiled path above) and
+    the calibration-probe surrogate (tiled fp64 path) vs the NumPy oracle."""
+    from paper_2508_09208_b200 import kernels
+    rng = np.random.default_rng(E)
+    D, n, B = 5_000, 3, 4
+    P = rng.normal(size=(E, D)) * 0.05
+    probes = rng.normal(size=(n, D))
+    proj = rng.normal(size=(B, D))
+    Pd = torch.as_tensor(P, device="cuda")
+    sim, _, _ = kernels.similarity([Pd[e] for e in range(E)], None, None, 1.0)
+    np.testing.assert_allclose(sim.cpu().numpy(), M.cosine_matrix(P), rtol=1e-9, atol=1e-12)
+    sim, _, _ = kernels.similarity([Pd[e] for e in range(E)], torch.as_tensor(probes, device="cuda"),
+                                   torch.as_tensor(proj, device="cuda"), 0.5)
+    np.testing.assert_allclose(sim.cpu().numpy(), M.similarity(P, probes, proj, 0.5), rtol=1e-9,
+                               atol=1e-9)
+
+
+def test_merge_many_groups_unstaged_path():
+    """More groups than the shared-memory group table holds (1024): the
+    kernel falls back to global group/weight lookups; results unchanged."""
+    from paper_2508_09208_b200 import kernels
+    G, D = 1100, 4096
+    g = torch.Generator(device="cuda").manual_seed(3)
+    V = (torch.randn(G + 1, D, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+    outs = [torch.empty(D, dtype=torch.bfloat16, device="cuda") for _ in range(G)]
+    members = [[V[i], V[i + 1]] for i in range(G)]
+    w = [[1.0 + (i % 3), 2.0] for i in range(G)]
+    kernels.merge_groups(members, w, [sum(x) for x in w], outs, torch.bfloat16)
+    Vf = V.float()
+    for i in (0, 517, G - 1):
+        ref = (w[i][0] * Vf[i] + w[i][1] * Vf[i + 1]) / sum(w[i])
+        torch.testing.assert_close(outs[i].float(), ref, rtol=1e-2, atol=1e-4)
+
+
+@pytest.mark.parametrize("E,K", [(20, 1), (64, 2), (200, 2)])
+def test_predictor_expert_counts(E, K):
+    """Every experts-per-lane instantiation, duplicate K-hot slots and a
+    ragged last token chunk."""
+    from paper_2508_09208_b200 import kernels
+    rng = np.random.default_rng(E)
+    emb, ctx, H, B = 16, 8, 32, 777
+    w1 = rng.normal(scale=0.1, size=(H, E + emb + ctx)); b1 = rng.normal(size=H) * 0.1
+    w2 = rng.normal(scale=0.1, size=(E, H)); b2 = rng.normal(size=E) * 0.1
+    slots = rng.integers(0, E, size=(B, K)).astype(np.int32)
+    slots[::7, -1] = slots[::7, 0]  # duplicates count once
+    he = rng.normal(size=(B, emb)); ce = rng.normal(size=(B, ctx))
+    X = np.zeros((B, E + emb + ctx))
+    for k in range(K):
+        X[np.arange(B), slots[:, k]] = 1.0
+    X[:, E:E + emb] = he
+    X[:, E + emb:] = ce
+    z = np.maximum(X @ w1.T + b1, 0) @ w2.T + b2
+    z -= z.max(1, keepdims=True)
+    ref = np.exp(z) / np.exp(z).sum(1, keepdims=True)
+    d = lambda a: torch.as_tensor(a, device="cuda")
+    probs, demand = kernels.predictor_mlp(d(slots), d(he), d(ce), d(w1), d(b1), d(w2), d(b2),
+                                          want_demand=True)
+    np.testing.assert_allclose(probs.cpu().numpy(), ref, rtol=1e-10, atol=1e-13)
+    np.testing.assert_allclose(demand.cpu().numpy(), ref.sum(0), rtol=1e-10)
