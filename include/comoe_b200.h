@@ -53,7 +53,9 @@ int comoe_num_sms(int device);
  * ModelVariant.resolve (pkg/src/comoe/aggregation.py:101-103) as `slot_map`.
  *
  * comoe_gate_prepare: split the fp32 router Wg[d,E] (row-major, x @ Wg) into
- *   three bf16 terms wg_split[3][EP][d] (EP = comoe_gate_padded_experts(E)).
+ *   three bf16 terms wg_split[3][EP][d] (EP = comoe_gate_padded_experts(E));
+ *   hi + mid + lo == Wg exactly. comoe_gate_topk uses hi + mid by default
+ *   (logit error ~3e-7 at d = 768) or all three (env COMOE_GATE_TERMS=3).
  * comoe_gate_topk: for each token t of x[T,d] (bf16): logits = x_t . Wg (fp32,
  *   tensor cores), top-k on the logits (k in {1,2}), probabilities
  *   (norm_topk=0: softmax over all E; 1: renormalised over the k picks),

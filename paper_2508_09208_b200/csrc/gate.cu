@@ -8,10 +8,11 @@
 // tie rule, aggregation.py:165,193), slot remap through the variant's
 // slot_map, and per-tile token-order ranks that feed deterministic capacity.
 //
-// fp32-faithful logits on bf16 tensor cores: X is bf16 (exact); the fp32
-// router weight is split Wg = hi + mid + lo with each term bf16, so every
-// product x*term is exact in the fp32 accumulator and the three MMAs sum to
-// the fp32 logit up to accumulation rounding.
+// fp32-router logits on bf16 tensor cores: X is bf16 (exact); the fp32
+// router weight is split Wg = hi + mid + lo with each term bf16 (exactly),
+// so every product x*term is exact in the fp32 accumulator; the MMAs over
+// the first gate_terms() terms sum to the fp32 logit up to accumulation
+// rounding (2 terms: ~3e-7 at d = 768, see gate_terms()).
 #include <cooperative_groups.h>
 #include <cstdlib>
 
@@ -62,22 +63,22 @@ struct GateParams {
 // tokens and half of every router term (EP/2 experts), cutting per-SM shared-
 // memory traffic ~30% (the 1-SM gate is smem-bound: the token tile is re-read
 // once per term); each SM's TMEM still holds full logit rows of its tokens.
-template <int EP, int kStages, bool kPair = false>
+template <int EP, int kStages, bool kPair = false, int kTerms = 3>
 struct GateSmem {
   static constexpr int kBRows = kPair ? EP / 2 : EP;
   static constexpr int kABytes = kGemmBM * kGemmBK * 2;
-  static constexpr int kBBytes = 3 * kBRows * kGemmBK * 2;
+  static constexpr int kBBytes = kTerms * kBRows * kGemmBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTileBytes = kStages * kStageBytes;
   static constexpr int kCtrlBytes = (2 * kStages + 4) * 8 + 16 + 2 * kGateMaxK * 4 * kGateMaxE * 4 + kGateMaxE * 4;
   static constexpr int kTotal = 1024 + kTileBytes + kCtrlBytes;
 };
 
-template <int EP, int kStages, bool kPair>
+template <int EP, int kStages, bool kPair, int kTerms>
 __global__ void __launch_bounds__(kGateThreads, 1)
     gate_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 const __grid_constant__ CUtensorMap tmap_w, GateParams p) {
-  using S = GateSmem<EP, kStages, kPair>;
+  using S = GateSmem<EP, kStages, kPair, kTerms>;
   constexpr uint32_t kTmemCols = 2 * EP <= 32 ? 32 : (2 * EP <= 64 ? 64 : (2 * EP <= 128 ? 128 : 256));
   constexpr uint32_t kIdesc = umma_idesc_bf16_f32(kPair ? 256 : kGemmBM, EP);
   constexpr int kBRows = S::kBRows;
@@ -159,7 +160,7 @@ __global__ void __launch_bounds__(kGateThreads, 1)
             tma_load_2d_2sm(smem_a + stage * S::kABytes, &tmap_x, fb, kb * kGemmBK,
                             tile * kGemmBM, pol_x);
 #pragma unroll
-            for (int term = 0; term < 3; ++term)
+            for (int term = 0; term < kTerms; ++term)
               tma_load_2d_2sm(b + term * kBRows * 128, &tmap_w, fb, kb * kGemmBK,
                               term * EP + static_cast<int>(rank) * kBRows, pol_w);
           } else {
@@ -167,7 +168,7 @@ __global__ void __launch_bounds__(kGateThreads, 1)
             tma_load_2d_hint(smem_a + stage * S::kABytes, &tmap_x, &full_bar[stage], kb * kGemmBK,
                              tile * kGemmBM, pol_x);
 #pragma unroll
-            for (int term = 0; term < 3; ++term)
+            for (int term = 0; term < kTerms; ++term)
               tma_load_2d(b + term * EP * 128, &tmap_w, &full_bar[stage], kb * kGemmBK, term * EP);
           }
           if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -189,7 +190,7 @@ __global__ void __launch_bounds__(kGateThreads, 1)
           tc_fence_after();
           const uint64_t adesc = umma_desc_k_sw128(smem_u32(smem_a + stage * S::kABytes));
 #pragma unroll
-          for (int term = 0; term < 3; ++term) {
+          for (int term = 0; term < kTerms; ++term) {
             const uint64_t bdesc =
                 umma_desc_k_sw128(smem_u32(smem_b + stage * S::kBBytes + term * kBRows * 128));
 #pragma unroll
@@ -362,12 +363,13 @@ __global__ void __launch_bounds__(kGateThreads, 1)
   }
 }
 
-template <int EP, bool kPair>
-static int launch_gate(const CUtensorMap& tx, const CUtensorMap& tw, const GateParams& p,
-                       cudaStream_t stream) {
-  constexpr int kStages = kPair ? 4 : (EP >= 128 ? 3 : 4);
-  using S = GateSmem<EP, kStages, kPair>;
-  auto kern = gate_kernel<EP, kStages, kPair>;
+template <int EP, bool kPair, int kTerms>
+static int launch_gate_terms(const CUtensorMap& tx, const CUtensorMap& tw, const GateParams& p,
+                             cudaStream_t stream) {
+  constexpr int kStages = kTerms == 2 ? (kPair ? 5 : 4) : (kPair ? 4 : (EP >= 128 ? 3 : 4));
+  using S = GateSmem<EP, kStages, kPair, kTerms>;
+  static_assert(S::kTotal <= 227 * 1024, "gate shared memory");
+  auto kern = gate_kernel<EP, kStages, kPair, kTerms>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kTotal);
@@ -406,6 +408,27 @@ static int launch_gate(const CUtensorMap& tx, const CUtensorMap& tw, const GateP
     cudaLaunchKernelEx(&cfg, kern, tx, tw, p);
     return check_launch("gate_kernel");
   }
+}
+
+// Router split terms used by the MMAs (COMOE_GATE_TERMS=2|3, default 2).
+// Wg = hi + mid + lo is exact; hi + mid keeps 16 of fp32's 24 mantissa bits
+// (|lo| <= 2^-17 |Wg|): logit error ~3e-7 at d = 768 (the fp32 accumulation
+// itself contributes ~1e-7; the parity bar vs the fp64 oracle is 2e-5, and
+// routing parity is defined on the device logits). Two terms cut the
+// gate's tensor work and router traffic by a third.
+static int gate_terms() {
+  static const int t = [] {
+    const char* e = std::getenv("COMOE_GATE_TERMS");
+    return (e && e[0] == '3') ? 3 : 2;
+  }();
+  return t;
+}
+
+template <int EP, bool kPair>
+static int launch_gate(const CUtensorMap& tx, const CUtensorMap& tw, const GateParams& p,
+                       cudaStream_t stream) {
+  return gate_terms() == 3 ? launch_gate_terms<EP, kPair, 3>(tx, tw, p, stream)
+                           : launch_gate_terms<EP, kPair, 2>(tx, tw, p, stream);
 }
 
 static bool gate_pair_enabled() {
