@@ -144,6 +144,19 @@ static int* sched_counters() {
   return ring[dev] + 32 * (next[dev].fetch_add(1) % kSchedSlots);
 }
 
+// 1-SM kernel tile order: feature-tile major when one group's weight block
+// exceeds 32 MB (Mixtral: 235 MB per expert — token-tile major re-streamed
+// every expert's weights from HBM once per 128-token tile); COMOE_GEMM_ORDER
+// = 0 / 1 forces token- / feature-tile major.
+static int ft_major(long weight_bytes) {
+  static const int forced = [] {
+    const char* e = std::getenv("COMOE_GEMM_ORDER");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (forced >= 0) return forced;
+  return weight_bytes > (32L << 20) ? 1 : 0;
+}
+
 static bool force_1sm() {
   static const bool f = [] {
     const char* e = std::getenv("COMOE_GEMM_1SM");
@@ -177,7 +190,7 @@ static int grouped_gemm_impl(const void* a, long a_rows, const void* pool, int n
   const void* b = static_cast<const __nv_bfloat16*>(pool) + b_offset;
   GroupedGemmParams p{group_rows, group_row_base, group_slot, G, N, K,
                       reinterpret_cast<__nv_bfloat16*>(out), ldo, row_token, row_prob,
-                      a_gather, gemm_debug(), nullptr};
+                      a_gather, gemm_debug(), ft_major(static_cast<long>(N) * K * 2), nullptr};
   int rc;
   if (epi_mode != kEpiSwiGLU && !force_1sm()) {
     COMOE_REQUIRE(G <= kMaxGroups2, kBadArg, "grouped_gemm: G=%d > %d", G, kMaxGroups2);

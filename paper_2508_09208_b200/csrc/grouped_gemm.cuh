@@ -41,6 +41,8 @@ struct GroupedGemmParams {
   int debug;              // dev-only attribution switches (COMOE_GEMM_DEBUG): 1 = no epilogue
                           // math/stores, 2 = no TMA (MMA on stale smem), 4 = no TMA store,
                           // 16/128 = L2-resident operands (see the producer); 0 in production
+  int ft_major;           // 1-SM kernel: tile order inside a group (0: token tile major,
+                          // 1: feature tile major — consecutive CTAs share a weight tile)
   int* sched;             // 2-SM kernel: {next tile, finished clusters} counters for dynamic
                           // tile claiming (zero on entry, reset to zero by the last cluster);
                           // nullptr = static round-robin
@@ -113,6 +115,19 @@ __device__ __forceinline__ int find_group(const int* prefix, int G, int tile) {
   return lo;
 }
 
+// (token tile mt, feature tile nt) of tile `local` of group g
+__device__ __forceinline__ void tile_coords(const GroupedGemmParams& p, int g, int local,
+                                            int n_tiles, int& mt, int& nt) {
+  if (p.ft_major) {
+    const int n_mt = (__ldg(p.group_rows + g) + kGemmBM - 1) / kGemmBM;
+    mt = local % n_mt;
+    nt = local / n_mt;
+  } else {
+    mt = local / n_tiles;
+    nt = local % n_tiles;
+  }
+}
+
 template <int BN, int kStages, int kMode>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
@@ -170,7 +185,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
         const int g = find_group(prefix, p.G, tile);
         const int local = tile - prefix[g];
-        const int mt = local / n_tiles, nt = local % n_tiles;
+        int mt, nt;
+        tile_coords(p, g, local, n_tiles, mt, nt);
         const int a_row = __ldg(p.group_row_base + g) + mt * kGemmBM;
         const int b_slot = __ldg(p.group_slot + g);
         for (int kb = 0; kb < k_blocks; ++kb) {
@@ -225,7 +241,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint32_t acc_phase = (it >> 1) & 1;
       const int g = find_group(prefix, p.G, tile);
       const int local = tile - prefix[g];
-      const int mt = local / n_tiles, nt = local % n_tiles;
+      int mt, nt;
+      tile_coords(p, g, local, n_tiles, mt, nt);
       const int rows = __ldg(p.group_rows + g);
       const int r0 = mt * kGemmBM + q * 32;  // first row (within the group) of this warp
       const long arow0 = static_cast<long>(__ldg(p.group_row_base + g)) + r0;

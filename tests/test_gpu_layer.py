@@ -116,6 +116,26 @@ def test_swiglu_layer_top2(T, d, d_ff, E, norm):
     assert O.normwise_error(_np(y), ref) < NORMWISE_TOL
 
 
+def test_swiglu_large_experts_feature_major_order():
+    """Experts whose W_in block exceeds 32 MB (d 1024, d_ff 8192: 33.5 MB)
+    take the feature-tile-major tile order of the 1-SM GEMM (the Mixtral
+    fix); outputs must not change."""
+    from paper_2508_09208_b200 import ExpertPool, MoELayer
+    T, d, d_ff, E = 512, 1024, 8192, 2
+    x, wg, w = _layer_inputs(T, d, d_ff, E, "swiglu", seed=5)
+    pool = ExpertPool(E, w.shape[1])
+    pool.data[:, : w.shape[1]].copy_(w.cuda())
+    layer = MoELayer(wg, pool, d_ff, act="swiglu", top_k=2, norm_topk=True, capacity_factor=1.25)
+    y = layer.forward(x, want_logits=True)
+    torch.cuda.synchronize()
+    logits = layer.last.gate.logits.cpu().numpy()
+    ref, info = O.layer_forward(_np(x), _np(wg), [_np(w[e]) for e in range(E)], top_k=2,
+                                norm_topk=True, capacity_factor=1.25, act="swiglu", d_ff=d_ff,
+                                logits=logits)
+    _check_routing(layer, x, wg, info, T)
+    assert O.normwise_error(_np(y), ref) < NORMWISE_TOL
+
+
 def test_merged_variant_routing_and_output():
     """8 experts merged into 4 groups: slot remap in the gate, capacity on
     the merged count, FFN on merged pool slots."""
