@@ -8,6 +8,8 @@
 // computed in 32x32 output tiles over D-slices, then reduced over slices in a
 // fixed order (deterministic). Always accumulated in fp64 (the reference is
 // fp64 and its surrogate softmax is sensitive to logit error).
+#include <utility>
+
 #include "common.cuh"
 #include "../../include/comoe_b200.h"
 
@@ -303,6 +305,140 @@ __global__ void __launch_bounds__(128) sim_gram_mma_kernel(const void* const* __
       }
 }
 
+// Surrogate logits for E <= 8 experts and <= 8 buckets (the reference's
+// defaults): logits[e][n][b] = sum_d P[e,d] probes[n,d] proj[b,d]. A block
+// owns a contiguous D-slice and streams it in 256-d chunks through a
+// double-buffered cp.async pipeline (expert rows, up to 8 probe rows, the
+// projection rows), so DRAM latency overlaps the fp64 math; warp w takes
+// probe n0 + w, lane = d inside the chunk, 64 fp64 accumulators (e, b) per
+// lane, u_e = P[e,d]*probe formed once per (e, d). Lane partials are
+// tree-reduced per warp and written per block (deterministic). Replaces the
+// 16x64-tile fp64 path for this shape, where 72% of the FMAs hit padding
+// and every column re-read its probe and projection rows (7.8 ms at C1).
+constexpr int kLogitE = 8, kLogitB = 8, kLogitN = 8, kLogitChunk = 256;
+
+template <typename T>
+struct LogitStage {
+  static constexpr int kPBytes = kLogitE * kLogitChunk * static_cast<int>(sizeof(T));
+  static constexpr int kQBytes = kLogitN * kLogitChunk * 8;  // probes
+  static constexpr int kRBytes = kLogitB * kLogitChunk * 8;  // projection
+  static constexpr int kBytes = kPBytes + kQBytes + kRBytes;
+};
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+
+constexpr int kLogitEW = 4;  // experts per warp: two warps per probe, 16 warps per block
+
+template <typename T>
+__global__ void __launch_bounds__(512) sim_logits_small_kernel(
+    const void* const* __restrict__ rows, int E, long D, const double* __restrict__ probes,
+    int n_probes, const double* __restrict__ proj, int B, long slice,
+    double* __restrict__ partial) {
+  using L = LogitStage<T>;
+  extern __shared__ __align__(16) uint8_t lsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long d0 = blockIdx.x * slice;
+  const long d1 = d0 + slice < D ? d0 + slice : D;
+  constexpr int kVecT = 16 / sizeof(T);  // row elements per 16-byte copy
+  for (int n0 = 0; n0 < n_probes; n0 += kLogitN) {
+    const int np = n_probes - n0 < kLogitN ? n_probes - n0 : kLogitN;
+    auto issue = [&](long c, int buf) {  // chunk starting at d = c into stage buf
+      uint8_t* st = lsm + buf * L::kBytes;
+      constexpr int kPV = kLogitChunk / kVecT, kDV = kLogitChunk / 2;  // 16-B vectors per row
+      for (int i = threadIdx.x; i < E * kPV + (np + B) * kDV; i += blockDim.x) {
+        if (i < E * kPV) {
+          const int e = i / kPV, v = i % kPV;
+          const long d = c + static_cast<long>(v) * kVecT;
+          cp_async16(st + (e * kLogitChunk + v * kVecT) * sizeof(T),
+                     static_cast<const T*>(rows[e]) + (d < d1 ? d : 0), d < d1);
+        } else {
+          const int j = i - E * kPV;
+          const int r = j / kDV, v = j % kDV;
+          const long d = c + 2L * v;
+          const double* src = r < np ? probes + static_cast<long>(n0 + r) * D
+                                     : proj + static_cast<long>(r - np) * D;
+          uint8_t* dst = st + L::kPBytes + (r < np ? r * kLogitChunk * 8
+                                                   : L::kQBytes + (r - np) * kLogitChunk * 8);
+          cp_async16(dst + v * 16, src + (d < d1 ? d : 0), d < d1);
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    // warp w: probe n0 + (w & 7), experts e0 .. e0 + kLogitEW - 1 with e0 = (w >> 3) * kLogitEW
+    const int wn = warp & 7, e0 = (warp >> 3) * kLogitEW;
+    const bool active = wn < np && e0 < E;
+    double acc[kLogitEW][kLogitB];
+#pragma unroll
+    for (int e = 0; e < kLogitEW; ++e)
+#pragma unroll
+      for (int b = 0; b < kLogitB; ++b) acc[e][b] = 0.0;
+    int buf = 0;
+    if (d0 < d1) issue(d0, 0);
+    for (long c = d0; c < d1; c += kLogitChunk, buf ^= 1) {
+      if (c + kLogitChunk < d1) {
+        issue(c + kLogitChunk, buf ^ 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
+      __syncthreads();
+      const uint8_t* st = lsm + buf * L::kBytes;
+      const T* ps = reinterpret_cast<const T*>(st);
+      const double* qs = reinterpret_cast<const double*>(st + L::kPBytes);
+      const double* rs = reinterpret_cast<const double*>(st + L::kPBytes + L::kQBytes);
+      if (active) {
+#pragma unroll 2
+        for (int i = 0; i < kLogitChunk / 32; ++i) {
+          const int dd = lane + 32 * i;  // (rows past d1 were zero-filled)
+          const double pr = qs[wn * kLogitChunk + dd];
+          double q[kLogitB];
+#pragma unroll
+          for (int b = 0; b < kLogitB; ++b) q[b] = b < B ? rs[b * kLogitChunk + dd] : 0.0;
+#pragma unroll
+          for (int e = 0; e < kLogitEW; ++e) {
+            if (e0 + e >= E) break;
+            const double u = to_f64(ps[(e0 + e) * kLogitChunk + dd]) * pr;
+#pragma unroll
+            for (int b = 0; b < kLogitB; ++b) acc[e][b] = fma(u, q[b], acc[e][b]);
+          }
+        }
+      }
+      __syncthreads();  // this stage is refilled by the next iteration's issue
+    }
+    if (active) {
+#pragma unroll
+      for (int e = 0; e < kLogitEW; ++e)
+#pragma unroll
+        for (int b = 0; b < kLogitB; ++b) {
+          double v = acc[e][b];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          if (lane == 0 && e0 + e < E && b < B)
+            partial[(static_cast<long>(blockIdx.x) * E + e0 + e) * n_probes * B + (n0 + wn) * B + b] = v;
+        }
+    }
+  }
+}
+
+// out[i] = sum over splits (in order) of partial[split][i]; one warp per entry
+__global__ void sim_sum_partials(const double* __restrict__ partial, int splits, long n,
+                                 double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const long warps = static_cast<long>(gridDim.x) * (blockDim.x >> 5);
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x >> 5) + (threadIdx.x >> 5); i < n;
+       i += warps) {
+    double s = 0.0;
+    for (int k = lane; k < splits; k += 32) s += partial[k * n + i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[i] = s;
+  }
+}
+
 // one warp per output entry: lanes stride the splits, fixed-order tree
 // (deterministic); skipped below-diagonal Gram tiles read the mirror.
 __global__ void sim_reduce_kernel(const double* __restrict__ partial, int splits, int E, int ncols,
@@ -371,6 +507,57 @@ __global__ void sim_finalize_kernel(const double* __restrict__ gram,
   }
 }
 
+// Same result, one block: the log-softmax (log p and p) of every (expert,
+// probe) row is computed once into shared memory, then threads sweep the
+// pairs — the per-pair kernel above recomputes both rows' log-softmax for
+// every pair (74 us at E = 8 on one 128-thread block). Identical operation
+// order per value, so bit-identical output.
+constexpr int kFinalizeThreads = 1024;
+__global__ void __launch_bounds__(kFinalizeThreads) sim_finalize_staged_kernel(
+    const double* __restrict__ gram, const double* __restrict__ logits, int E, int n_probes,
+    int buckets, double alpha, double* __restrict__ sim) {
+  extern __shared__ double fsm[];
+  const int R = E * n_probes;  // rows (expert, probe)
+  double* lp = fsm;                              // [R][buckets] log p
+  double* pp = fsm + static_cast<long>(R) * buckets;  // [R][buckets] p
+  for (int r = threadIdx.x; r < R; r += blockDim.x) {
+    const double* l = logits + static_cast<long>(r) * buckets;
+    double m = -INFINITY;
+    for (int k = 0; k < buckets; ++k) m = fmax(m, l[k]);
+    double sm = 0.0;
+    for (int k = 0; k < buckets; ++k) sm += exp(l[k] - m);
+    const double ls = m + log(sm);
+    for (int k = 0; k < buckets; ++k) {
+      const double v = l[k] - ls;
+      lp[r * buckets + k] = v;
+      pp[r * buckets + k] = exp(v);
+    }
+  }
+  __syncthreads();
+  const long pairs = static_cast<long>(E) * E;
+  for (long idx = threadIdx.x; idx < pairs; idx += blockDim.x) {
+    const int a = static_cast<int>(idx / E), b = static_cast<int>(idx % E);
+    const double cosv = gram[static_cast<long>(a) * E + b] /
+                        (sqrt(gram[static_cast<long>(a) * E + a]) * sqrt(gram[static_cast<long>(b) * E + b]));
+    double mean_kl = 0.0;
+    for (int n = 0; n < n_probes; ++n) {
+      const int ra = (a * n_probes + n) * buckets, rb = (b * n_probes + n) * buckets;
+      double kab = 0.0, kba = 0.0;
+      for (int k = 0; k < buckets; ++k) {
+        const double lpa = lp[ra + k], lpb = lp[rb + k];
+        const double pa = pp[ra + k], pb = pp[rb + k];
+        if (pa > 0.0) kab += pa * (lpa - lpb);
+        if (pb > 0.0) kba += pb * (lpb - lpa);
+      }
+      mean_kl += 0.5 * (kab + kba);
+    }
+    if (n_probes > 0) mean_kl /= n_probes;
+    double sf = 1.0 - mean_kl;
+    sf = sf < 0.0 ? 0.0 : (sf > 1.0 ? 1.0 : sf);
+    sim[idx] = alpha * cosv + (1.0 - alpha) * sf;
+  }
+}
+
 static int num_sms() {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -423,6 +610,22 @@ static int sim_splits(int E, int ncols, long D) {
   return static_cast<int>(splits);
 }
 
+// 16-byte cp.async of rows, probes and projection: D % 8 == 0 (bf16) / % 2 (f64)
+static bool sim_logits_small(int E, int buckets, long D) {
+  return E <= kLogitE && buckets <= kLogitB && D % 8 == 0;
+}
+
+// (d per block, blocks) of the small-logit kernel: one block per SM (register-bound)
+static std::pair<long, int> logit_plan(long D) {
+  long blocks = static_cast<long>(num_sms());
+  const long need = (D + 1023) / 1024;
+  if (blocks > need) blocks = need;
+  if (blocks < 1) blocks = 1;
+  // slices start on 256-d chunk boundaries (16-byte aligned cp.async sources)
+  const long slice = ((D + blocks - 1) / blocks + kLogitChunk - 1) / kLogitChunk * kLogitChunk;
+  return {slice, static_cast<int>((D + slice - 1) / slice)};
+}
+
 template <typename T>
 static void launch_small(int E, const void* const* rows, long D, int blocks, double* partial,
                          cudaStream_t s) {
@@ -438,70 +641,11 @@ static void launch_small(int E, const void* const* rows, long D, int blocks, dou
   }
 }
 
-}  // namespace comoe
-
-extern "C" {
-
-long comoe_sim_workspace_bytes(int E, int n_probes, int buckets, long D) {
-  // (bf16 and f64 share one workspace size: the larger of the two paths)
-  if (n_probes == 0 && D % 8 == 0) {
-    const comoe::GramPlan g = comoe::gram_plan(E, D);
-    long w = static_cast<long>(g.splits) * E * E * sizeof(double);
-    if (comoe::sim_small(E, n_probes)) {
-      const long ws = static_cast<long>(comoe::sim_small_blocks(D)) * (E * (E + 1) / 2) * sizeof(double);
-      w = w > ws ? w : ws;
-    } else {
-      const long wt = static_cast<long>(comoe::sim_splits(E, E, D)) * E * E * sizeof(double);
-      w = w > wt ? w : wt;
-    }
-    return w;
-  }
-  if (comoe::sim_small(E, n_probes))
-    return static_cast<long>(comoe::sim_small_blocks(D)) * (E * (E + 1) / 2) * sizeof(double);
-  const int ncols = E + (n_probes > 0 ? n_probes * buckets : 0);
-  return static_cast<long>(comoe::sim_splits(E, ncols, D)) * E * ncols * sizeof(double);
-}
-
-int comoe_sim_contract(int dtype, const void* const* rows, int E, long D, const double* probes,
-                       int n_probes, const double* proj, int buckets, double* gram,
-                       double* logits, void* work, void* stream) {
-  using namespace comoe;
-  COMOE_REQUIRE(rows && gram && work, kBadArg, "sim_contract: null pointer");
-  COMOE_REQUIRE(n_probes == 0 || (probes && proj && logits && buckets >= 1), kBadArg,
-                "sim_contract: null calibration");
-  COMOE_REQUIRE(E >= 1 && D >= 1 && n_probes >= 0, kBadArg, "sim_contract: bad sizes");
-  COMOE_REQUIRE(dtype == COMOE_DTYPE_BF16 || dtype == COMOE_DTYPE_F64, kBadArg,
-                "sim_contract: dtype %d", dtype);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  double* partial = static_cast<double*>(work);
-  if (sim_mma(dtype, n_probes, D)) {
-    const GramPlan gp = gram_plan(E, D);
-    const long units = static_cast<long>(gp.tiles_1d) * (gp.tiles_1d + 1) / 2 * gp.splits;
-    const unsigned nb = static_cast<unsigned>((units + 3) / 4);
-    if (E <= 8)
-      sim_gram_mma_kernel<1, 8><<<nb, 128, 0, s>>>(rows, E, D, gp.tiles_1d, gp.splits, gp.slice,
-                                                   partial);
-    else
-      sim_gram_mma_kernel<4, 1><<<nb, 128, 0, s>>>(rows, E, D, gp.tiles_1d, gp.splits, gp.slice,
-                                                   partial);
-    int rc = check_launch("sim_gram_mma_kernel");
-    if (rc) return rc;
-    const long n = static_cast<long>(E) * E;
-    const int blocks = static_cast<int>((n + 7) / 8 < 4096 ? (n + 7) / 8 : 4096);
-    sim_reduce_kernel<<<blocks, 256, 0, s>>>(partial, gp.splits, E, E, gram_tile(E), gram, nullptr);
-    return check_launch("sim_reduce_kernel");
-  }
-  if (sim_small(E, n_probes)) {
-    // rows must be 16-byte aligned for the vector loads (pool slots and
-    // torch allocations are)
-    const int blocks = sim_small_blocks(D);
-    if (dtype == COMOE_DTYPE_BF16) launch_small<__nv_bfloat16>(E, rows, D, blocks, partial, s);
-    else launch_small<double>(E, rows, D, blocks, partial, s);
-    int rc = check_launch("sim_gram_small_kernel");
-    if (rc) return rc;
-    sim_gram_small_reduce<<<1, 64, 0, s>>>(partial, blocks, E, gram);
-    return check_launch("sim_gram_small_reduce");
-  }
+// One fp64 tiled pass over [E] x [E + n*B] columns: the Gram and (with
+// probes) the surrogate logits.
+static int tiled_contract(int dtype, const void* const* rows, int E, long D, const double* probes,
+                          int n_probes, const double* proj, int buckets, double* gram,
+                          double* logits, double* partial, cudaStream_t s) {
   if (n_probes == 0) buckets = 0;  // cosine only
   const int ncols = E + n_probes * buckets;
   const int splits = sim_splits(E, ncols, D);
@@ -532,12 +676,122 @@ int comoe_sim_contract(int dtype, const void* const* rows, int E, long D, const 
   return check_launch("sim_reduce_kernel");
 }
 
+// Cosine Gram only (tensor cores for bf16, register path for small f64 E,
+// fp64 tiles otherwise) into gram[E,E]
+static int gram_contract(int dtype, const void* const* rows, int E, long D, double* gram,
+                         double* partial, cudaStream_t s) {
+  if (sim_mma(dtype, 0, D)) {
+    const GramPlan gp = gram_plan(E, D);
+    const long units = static_cast<long>(gp.tiles_1d) * (gp.tiles_1d + 1) / 2 * gp.splits;
+    const unsigned nb = static_cast<unsigned>((units + 3) / 4);
+    if (E <= 8)
+      sim_gram_mma_kernel<1, 8><<<nb, 128, 0, s>>>(rows, E, D, gp.tiles_1d, gp.splits, gp.slice,
+                                                   partial);
+    else
+      sim_gram_mma_kernel<4, 1><<<nb, 128, 0, s>>>(rows, E, D, gp.tiles_1d, gp.splits, gp.slice,
+                                                   partial);
+    int rc = check_launch("sim_gram_mma_kernel");
+    if (rc) return rc;
+    const long n = static_cast<long>(E) * E;
+    const int blocks = static_cast<int>((n + 7) / 8 < 4096 ? (n + 7) / 8 : 4096);
+    sim_reduce_kernel<<<blocks, 256, 0, s>>>(partial, gp.splits, E, E, gram_tile(E), gram, nullptr);
+    return check_launch("sim_reduce_kernel");
+  }
+  if (sim_small(E, 0)) {
+    // rows must be 16-byte aligned for the vector loads (pool slots and
+    // torch allocations are)
+    const int blocks = sim_small_blocks(D);
+    if (dtype == COMOE_DTYPE_BF16) launch_small<__nv_bfloat16>(E, rows, D, blocks, partial, s);
+    else launch_small<double>(E, rows, D, blocks, partial, s);
+    int rc = check_launch("sim_gram_small_kernel");
+    if (rc) return rc;
+    sim_gram_small_reduce<<<1, 64, 0, s>>>(partial, blocks, E, gram);
+    return check_launch("sim_gram_small_reduce");
+  }
+  return tiled_contract(dtype, rows, E, D, nullptr, 0, nullptr, 0, gram, nullptr, partial, s);
+}
+
+}  // namespace comoe
+
+extern "C" {
+
+long comoe_sim_workspace_bytes(int E, int n_probes, int buckets, long D) {
+  using namespace comoe;
+  if (n_probes > 0 && !sim_logits_small(E, buckets, D)) {
+    const int ncols = E + n_probes * buckets;
+    return static_cast<long>(sim_splits(E, ncols, D)) * E * ncols * sizeof(double);
+  }
+  // Gram path (bf16 and f64 share one size: the larger), plus the small-logit partials
+  long w = static_cast<long>(sim_splits(E, E, D)) * E * E * sizeof(double);
+  if (D % 8 == 0) {
+    const GramPlan g = gram_plan(E, D);
+    const long wm = static_cast<long>(g.splits) * E * E * sizeof(double);
+    w = w > wm ? w : wm;
+  }
+  if (sim_small(E, 0)) {
+    const long ws = static_cast<long>(sim_small_blocks(D)) * (E * (E + 1) / 2) * sizeof(double);
+    w = w > ws ? w : ws;
+  }
+  if (n_probes > 0) w += logit_plan(D).second * static_cast<long>(E) * n_probes * buckets * sizeof(double);
+  return w;
+}
+
+int comoe_sim_contract(int dtype, const void* const* rows, int E, long D, const double* probes,
+                       int n_probes, const double* proj, int buckets, double* gram,
+                       double* logits, void* work, void* stream) {
+  using namespace comoe;
+  COMOE_REQUIRE(rows && gram && work, kBadArg, "sim_contract: null pointer");
+  COMOE_REQUIRE(n_probes == 0 || (probes && proj && logits && buckets >= 1), kBadArg,
+                "sim_contract: null calibration");
+  COMOE_REQUIRE(E >= 1 && D >= 1 && n_probes >= 0, kBadArg, "sim_contract: bad sizes");
+  COMOE_REQUIRE(dtype == COMOE_DTYPE_BF16 || dtype == COMOE_DTYPE_F64, kBadArg,
+                "sim_contract: dtype %d", dtype);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double* partial = static_cast<double*>(work);
+  if (n_probes > 0 && !sim_logits_small(E, buckets, D))  // one tiled pass: Gram and logits
+    return tiled_contract(dtype, rows, E, D, probes, n_probes, proj, buckets, gram, logits,
+                          partial, s);
+  int rc = gram_contract(dtype, rows, E, D, gram, partial, s);
+  if (rc || n_probes == 0) return rc;
+  // small surrogate logits, partials after the Gram's (stream order keeps them apart)
+  const std::pair<long, int> lp = logit_plan(D);
+  double* lpart = partial + (comoe_sim_workspace_bytes(E, n_probes, buckets, D) / sizeof(double) -
+                             static_cast<long>(lp.second) * E * n_probes * buckets);
+  if (dtype == COMOE_DTYPE_BF16) {
+    constexpr int smem = 2 * LogitStage<__nv_bfloat16>::kBytes;
+    cudaFuncSetAttribute(sim_logits_small_kernel<__nv_bfloat16>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    sim_logits_small_kernel<__nv_bfloat16><<<lp.second, 512, smem, s>>>(
+        rows, E, D, probes, n_probes, proj, buckets, lp.first, lpart);
+  } else {
+    constexpr int smem = 2 * LogitStage<double>::kBytes;
+    cudaFuncSetAttribute(sim_logits_small_kernel<double>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    sim_logits_small_kernel<double><<<lp.second, 512, smem, s>>>(rows, E, D, probes, n_probes,
+                                                                 proj, buckets, lp.first, lpart);
+  }
+  rc = check_launch("sim_logits_small_kernel");
+  if (rc) return rc;
+  const long n = static_cast<long>(E) * n_probes * buckets;
+  sim_sum_partials<<<static_cast<int>((n + 7) / 8), 256, 0, s>>>(lpart, lp.second, n, logits);
+  return check_launch("sim_sum_partials");
+}
+
 int comoe_sim_finalize(const double* gram, const double* logits, int E, int n_probes, int buckets,
                        double alpha, double* sim, void* stream) {
   using namespace comoe;
   COMOE_REQUIRE(gram && sim && (logits || n_probes == 0), kBadArg, "sim_finalize: null pointer");
   COMOE_REQUIRE(alpha >= 0.0 && alpha <= 1.0, kBadArg, "sim_finalize: alpha=%g", alpha);
   const long pairs = static_cast<long>(E) * E;
+  const long smem = 2L * E * n_probes * buckets * static_cast<long>(sizeof(double));
+  if (n_probes > 0 && smem <= 200 * 1024) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(sim_finalize_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem));
+    sim_finalize_staged_kernel<<<1, kFinalizeThreads, smem, static_cast<cudaStream_t>(stream)>>>(
+        gram, logits, E, n_probes, buckets, alpha, sim);
+    return check_launch("sim_finalize_staged_kernel");
+  }
   const int blocks = static_cast<int>((pairs + 127) / 128 < 1024 ? (pairs + 127) / 128 : 1024);
   sim_finalize_kernel<<<blocks, 128, 0, static_cast<cudaStream_t>(stream)>>>(
       gram, logits, E, n_probes, buckets, alpha, sim);

@@ -150,6 +150,15 @@ def main():
     ms = timed(lambda: kernels.similarity(rows8, None, None, 1.0))
     line("similarity cosine (K6, E=8)", ms, 8 * numel * 2, "E*D*2", flops=2 * 8 * 8 * numel)
 
+    # K6 with the reference's functional surrogate at C1 (E=8, 8 probes x 8
+    # buckets over D): bytes = rows (bf16) + probes + projection (fp64)
+    probes = torch.randn(8, numel, device=dev, dtype=torch.float64, generator=g)
+    proj = torch.randn(8, numel, device=dev, dtype=torch.float64, generator=g)
+    ms = timed(lambda: kernels.similarity(rows8, probes, proj, 0.5), reps=5)
+    line("similarity + surrogate (K6, E=8, 8x8 probes)", ms, 8 * numel * 2 + 16 * numel * 8,
+         "E*D*2 + (n+B)*D*8", flops=2 * 8 * (8 + 64 + 8) * numel)
+    del probes, proj
+
     # K8 predictor over 65,536 tokens (E=128, emb 16, ctx 8, hidden 32)
     hid = 32
     w1 = torch.randn(hid, E + 24, device=dev, dtype=torch.float64) * 0.1
