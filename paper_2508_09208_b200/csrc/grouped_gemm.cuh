@@ -41,7 +41,7 @@ struct GroupedGemmParams {
   int debug;              // dev-only attribution switches (COMOE_GEMM_DEBUG): 1 = no epilogue
                           // math/stores, 2 = no TMA (MMA on stale smem), 4 = no TMA store,
                           // 16/128 = L2-resident operands (see the producer); 0 in production
-  int ft_major;           // 1-SM kernel: tile order inside a group (0: token tile major,
+  int ft_major;           // tile order inside a group (0: token tile major,
                           // 1: feature tile major — consecutive CTAs share a weight tile)
   int* sched;             // 2-SM kernel: {next tile, finished clusters} counters for dynamic
                           // tile claiming (zero on entry, reset to zero by the last cluster);
@@ -276,8 +276,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             for (int j = 0; j < 16; ++j) {
               const float g0 = __uint_as_float(gv[2 * j]), g1 = __uint_as_float(gv[2 * j + 1]);
               const float u0 = __uint_as_float(uv[2 * j]), u1 = __uint_as_float(uv[2 * j + 1]);
-              packed[16 * h + j] = pack_bf16x2(g0 / (1.f + __expf(-g0)) * u0,
-                                               g1 / (1.f + __expf(-g1)) * u1);
+              packed[16 * h + j] = pack_bf16x2(__fdividef(g0, 1.f + __expf(-g0)) * u0,
+                                               __fdividef(g1, 1.f + __expf(-g1)) * u1);
             }
           }
         } else {

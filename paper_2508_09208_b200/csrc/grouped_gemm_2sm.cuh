@@ -243,8 +243,15 @@ __device__ __forceinline__ Tile2 decode_tile2(const int* prefix, const GroupedGe
   t.g = find_group(prefix, p.G, tile);
   const int local = tile - prefix[t.g];
   const int rows = __ldg(p.group_rows + t.g);
-  const int tt = local / f_tiles;
-  t.ft = local % f_tiles;
+  int tt;
+  if (p.ft_major) {  // big weight blocks: neighbouring pairs share a weight tile
+    const int n_tt = (rows + kTokTile - 1) / kTokTile;
+    tt = local % n_tt;
+    t.ft = local / n_tt;
+  } else {
+    tt = local / f_tiles;
+    t.ft = local % f_tiles;
+  }
   t.tok0 = tt * kTokTile;
   const int n = min(kTokTile, rows - t.tok0);
   t.ntok[0] = min(k2BN, n);
