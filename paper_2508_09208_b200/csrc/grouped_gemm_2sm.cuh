@@ -541,7 +541,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k
           __syncwarp();
           bool stored = false;
           if constexpr (kTmaStore) {
-            if (c + 32 <= ntok && !(p.debug & 4)) {  // (debug 4: dev, force st.global)  // whole chunk valid: one bulk tensor store
+            // whole chunk valid: one bulk tensor store (debug 4: dev, force st.global)
+            if (c + 32 <= ntok && !(p.debug & 4)) {
               fence_async_smem();
               __syncwarp();
               if (lane == 0) {
