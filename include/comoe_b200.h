@@ -174,9 +174,12 @@ int comoe_sim_finalize(const double* gram, const double* logits, int E, int n_pr
  * PredictorMLP.forward_batch (pkg/src/comoe/offload.py:147-154) with the
  * input built as in predict_next_layer (offload.py:157-172): x = [K-hot of
  * slots[t] over E | emb[t] | ctx[t]]; probs = softmax(W2 relu(W1 x + b1) + b2).
- * f64 throughout. demand[E] (optional) = sum_t probs[t]: token order within
- * fixed 256-token chunks, then chunk order (deterministic); it needs `work`
- * of comoe_predictor_workspace_bytes(B, E) bytes (unused when demand is NULL).
+ * f64 throughout. demand[E] (optional), reduced in token order within fixed
+ * 256-token chunks, then chunk order (deterministic): demand_mode 0 =
+ * sum_t probs[t] (expected picks), 1 = 1 - prod_t (1 - probs[t]) (the
+ * probability that some token of the batch picks the expert). It needs
+ * `work` of comoe_predictor_workspace_bytes(B, E) bytes (unused when demand
+ * is NULL).
  * The weights are staged in shared memory: (E+emb+ctx)*hidden + hidden*E
  * doubles (+ small terms) must fit 227 KB, else kUnsupportedShape.
  */
@@ -184,7 +187,7 @@ long comoe_predictor_workspace_bytes(int B, int E);
 int comoe_predictor_mlp(const int* slots, int B, int K, const double* emb, int emb_dim,
                         const double* ctx, int ctx_dim, const double* w1, const double* b1,
                         int hidden, const double* w2, const double* b2, int E, double* probs,
-                        double* demand, void* work, void* stream);
+                        double* demand, int demand_mode, void* work, void* stream);
 
 #ifdef __cplusplus
 }

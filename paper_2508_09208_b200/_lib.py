@@ -45,7 +45,7 @@ _SIGNATURES = {
     "comoe_sim_finalize": [_p, _p, _c_int, _c_int, _c_int, _c_double, _p, _p],
     "comoe_predictor_workspace_bytes": [_c_int, _c_int],
     "comoe_predictor_mlp": [_p, _c_int, _c_int, _p, _c_int, _p, _c_int, _p, _p, _c_int, _p,
-                            _p, _c_int, _p, _p, _p, _p],
+                            _p, _c_int, _p, _p, _c_int, _p, _p],
 }
 _RESTYPES = {"comoe_last_error": ctypes.c_char_p, "comoe_sim_workspace_bytes": _c_long,
              "comoe_predictor_workspace_bytes": _c_long}

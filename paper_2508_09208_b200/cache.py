@@ -339,17 +339,18 @@ class CachedMoELayer:
             raise ValueError(f"{G} groups but the cache holds {self.cache.E} experts")
         self.layer.set_variant(slot_map, [0] * G)  # slots come from the cache per wave
 
-    def forward(self, x, out=None, after_route=None):
+    def forward(self, x, out=None, after_route=None, routing=None):
         """`after_route(routing)` runs after the demand set is known and before
         the GEMMs are enqueued: the stack issues the next layer's prefetch
-        there so its copies overlap this layer's expert GEMMs."""
+        there so its copies overlap this layer's expert GEMMs. `routing` =
+        (expert_idx, probs) replays given choices (MoELayer.route)."""
         L = self.layer
         T = x.shape[0]
         if out is None:
             out = torch.empty((T, L.d), dtype=torch.bfloat16, device=x.device)
         ws = L._workspace(T)
         comp = torch.cuda.current_stream()
-        r = L.route(x)
+        r = L.route(x, routing=routing)
         k1 = L.top_k == 1
         kernels.permute(x, r.gate, r.scan, r.capacity, r.rows, y_zero=out if k1 else None,
                         out=r.perm)

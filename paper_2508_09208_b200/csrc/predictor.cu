@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(kPredWarps * 32, 2) predictor_kernel(
     const double* __restrict__ ctx, int ctx_dim, const double* __restrict__ w1,
     const double* __restrict__ b1, int hidden, const double* __restrict__ w2,
     const double* __restrict__ b2, int E, double* __restrict__ probs,
-    double* __restrict__ partial) {
+    double* __restrict__ partial, int demand_mode) {
   extern __shared__ double psm[];
   const int in_dim = E + emb_dim + ctx_dim;
   double* w1t = psm;                                        // [in_dim][hidden]
@@ -150,21 +150,25 @@ __global__ void __launch_bounds__(kPredWarps * 32, 2) predictor_kernel(
     if (partial) {
       __syncthreads();  // every token of the chunk written (block-visible)
       for (int e = threadIdx.x; e < E; e += blockDim.x) {
-        double s = 0.0;
-        for (int t = c * kPredChunk; t < t_end; ++t) s += probs[static_cast<long>(t) * E + e];
+        double s = 0.0;  // mode 0: sum_t p; mode 1: sum_t log(1 - p)
+        for (int t = c * kPredChunk; t < t_end; ++t) {
+          const double pt = probs[static_cast<long>(t) * E + e];
+          s += demand_mode ? log1p(-pt) : pt;
+        }
         partial[static_cast<long>(c) * E + e] = s;
       }
     }
   }
 }
 
-// demand[e] = sum over chunks (in order) of the chunk partials
+// demand[e] = sum over chunks (in order) of the chunk partials; mode 1
+// turns the summed log(1 - p) into P(some token of the batch picks e)
 __global__ void demand_kernel(const double* __restrict__ partial, int n_chunks, int E,
-                              double* __restrict__ demand) {
+                              int demand_mode, double* __restrict__ demand) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
     double s = 0.0;
     for (int c = 0; c < n_chunks; ++c) s += partial[static_cast<long>(c) * E + e];
-    demand[e] = s;
+    demand[e] = demand_mode ? -expm1(s) : s;
   }
 }
 
@@ -180,7 +184,7 @@ long comoe_predictor_workspace_bytes(int B, int E) {
 int comoe_predictor_mlp(const int* slots, int B, int K, const double* emb, int emb_dim,
                         const double* ctx, int ctx_dim, const double* w1, const double* b1,
                         int hidden, const double* w2, const double* b2, int E, double* probs,
-                        double* demand, void* work, void* stream) {
+                        double* demand, int demand_mode, void* work, void* stream) {
   using namespace comoe;
   COMOE_REQUIRE(slots && w1 && b1 && w2 && b2 && probs, kBadArg, "predictor: null pointer");
   COMOE_REQUIRE((emb_dim == 0 || emb) && (ctx_dim == 0 || ctx), kBadArg, "predictor: null emb/ctx");
@@ -189,12 +193,14 @@ int comoe_predictor_mlp(const int* slots, int B, int K, const double* emb, int e
   COMOE_REQUIRE(B >= 0 && K >= 1 && E >= 1 && emb_dim >= 0 && ctx_dim >= 0, kBadArg,
                 "predictor: bad sizes");
   COMOE_REQUIRE(!demand || work, kBadArg, "predictor: demand needs the workspace");
+  COMOE_REQUIRE(demand_mode == 0 || demand_mode == 1, kBadArg, "predictor: demand_mode=%d",
+                demand_mode);
   COMOE_REQUIRE(E <= 32 * kPredEPL, kUnsupportedShape, "predictor: E=%d > %d", E, 32 * kPredEPL);
   const long smem = pred_smem_bytes(E + emb_dim + ctx_dim, hidden, E);
   COMOE_REQUIRE(smem <= 227 * 1024, kUnsupportedShape,
                 "predictor: weights need %ld B of shared memory (> 227 KB)", smem);
   if (B == 0) {
-    if (demand) cudaMemsetAsync(demand, 0, sizeof(double) * E, static_cast<cudaStream_t>(stream));
+    if (demand) cudaMemsetAsync(demand, 0, sizeof(double) * E, static_cast<cudaStream_t>(stream));  // both modes: 0
     return check_launch("predictor(empty)");
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -209,7 +215,7 @@ int comoe_predictor_mlp(const int* slots, int B, int K, const double* emb, int e
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     kern<<<blocks, kPredWarps * 32, smem, s>>>(slots, B, K, emb, emb_dim, ctx, ctx_dim, w1, b1,
-                                                hidden, w2, b2, E, probs, partial);
+                                                hidden, w2, b2, E, probs, partial, demand_mode);
   };
   if (E <= 32) launch(predictor_kernel<1>);
   else if (E <= 64) launch(predictor_kernel<2>);
@@ -217,7 +223,7 @@ int comoe_predictor_mlp(const int* slots, int B, int K, const double* emb, int e
   else launch(predictor_kernel<8>);
   int rc = check_launch("predictor_kernel");
   if (rc || !demand) return rc;
-  demand_kernel<<<(E + 127) / 128, 128, 0, s>>>(partial, n_chunks, E, demand);
+  demand_kernel<<<(E + 127) / 128, 128, 0, s>>>(partial, n_chunks, E, demand_mode, demand);
   return check_launch("demand_kernel");
 }
 

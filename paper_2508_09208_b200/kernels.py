@@ -359,7 +359,9 @@ def similarity(rows, probes, proj, alpha):
 
 # ---------------------------------------------------------------- K8 predictor
 
-def predictor_mlp(slots, emb, ctx, w1, b1, w2, b2, want_demand=False):
+def predictor_mlp(slots, emb, ctx, w1, b1, w2, b2, want_demand=False, demand_mode="sum"):
+    """K8. demand_mode: "sum" = expected picks per expert over the batch,
+    "any" = probability that at least one token of the batch picks it."""
     _need(slots, "slots", torch.int32, 2)
     B, K = slots.shape
     for name, t in (("w1", w1), ("b1", b1), ("w2", w2), ("b2", b2)):
@@ -381,7 +383,7 @@ def predictor_mlp(slots, emb, ctx, w1, b1, w2, b2, want_demand=False):
         work = torch.empty(max(nbytes, 8), dtype=torch.uint8, device=slots.device)
     _lib.call("comoe_predictor_mlp", _ptr(slots), B, K, _ptr(emb), emb_dim, _ptr(ctx), ctx_dim,
               _ptr(w1), _ptr(b1), hidden, _ptr(w2), _ptr(b2), E, _ptr(probs), _ptr(demand),
-              _ptr(work), _stream())
+              {"sum": 0, "any": 1}[demand_mode], _ptr(work), _stream())
     return (probs, demand) if want_demand else probs
 
 

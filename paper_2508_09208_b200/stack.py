@@ -7,10 +7,13 @@ For each MoE layer l of the stack:
   1. route layer l (gate + scan) and serve its demand from cache_l (hits,
      substitutions, demand fetches — CachedMoELayer);
   2. if l is an encoder layer with a successor (simulator.py:709-712), run
-     the K8 predictor on layer l's routing for every token, reduce to the
-     expected per-expert demand of layer l+1 (mean probability over tokens,
-     the batched stand-in for the per-token probabilities the reference
-     passes to decide_prefetch), and prefetch into cache_{l+1} with the
+     the K8 predictor on layer l's routing for every token and reduce (in
+     K8) to the probability that layer l+1 demands each expert from this
+     batch, 1 - prod_t (1 - p_t) — the batched form of the per-token
+     probability the reference compares with the threshold in
+     decide_prefetch (a batch mean would wash out the peaked per-token
+     predictions: no expert ever crossed the threshold at 16-1024 tokens,
+     scripts/bench_stack.py) — and prefetch into cache_{l+1} with the
      resource-aware threshold. The copies run on cache_{l+1}'s copy stream
      and overlap layer l's grouped GEMMs;
   3. decoder layers can be pinned (pin_decoder, simulator.py:407-413).
@@ -44,19 +47,23 @@ class CachedMoEStack:
         self.theta = prefetch_threshold(self.policy, s_b, mem_avail, mem_total)
         self.prefetch_log = []
 
-    def forward(self, x, emb=None, ctx=None):
+    def forward(self, x, emb=None, ctx=None, routings=None):
         """x [T, d] bf16; emb/ctx [T, *] float64 device tensors for the
-        predictor (token embedding / context, as TokenRecord carries)."""
+        predictor (token embedding / context, as TokenRecord carries);
+        `routings` (optional, one (expert_idx, probs) per layer) replays a
+        routing trace instead of running each layer's router."""
         h = x
         for i, sl in enumerate(self.layers):
             nxt = self.layers[i + 1] if i + 1 < len(self.layers) else None
             hook = None
             if nxt is not None and sl.encoder and self.predictor is not None:
                 def hook(r, sl=sl, nxt=nxt):
-                    probs = self.predictor.predict_slots(r.gate.expert_idx, emb, ctx)
-                    demand = probs.mean(dim=0).cpu().numpy()
+                    _, demand = self.predictor.predict_slots(r.gate.expert_idx, emb, ctx,
+                                                             want_demand=True, demand_mode="any")
+                    demand = demand.cpu().numpy()
                     chosen = nxt.layer.cache.prefetch(demand, self.theta)
                     self.prefetch_log.append((sl.index, nxt.index, chosen))
-            y = sl.layer.forward(h, after_route=hook)
+            y = sl.layer.forward(h, after_route=hook,
+                                 routing=routings[i] if routings is not None else None)
             h = (y.float() + h.float()).to(torch.bfloat16)
         return h

@@ -220,3 +220,21 @@ def test_predictor_expert_counts(E, K):
                                           want_demand=True)
     np.testing.assert_allclose(probs.cpu().numpy(), ref, rtol=1e-10, atol=1e-13)
     np.testing.assert_allclose(demand.cpu().numpy(), ref.sum(0), rtol=1e-10)
+
+
+def test_predictor_any_demand_mode():
+    """demand_mode "any": 1 - prod_t (1 - p_t) per expert (the stack's
+    batched prefetch probability), across several 256-token chunks."""
+    from paper_2508_09208_b200 import kernels
+    rng = np.random.default_rng(3)
+    E, emb, ctx, H, B = 64, 16, 8, 32, 700
+    w1 = rng.normal(scale=0.3, size=(H, E + emb + ctx)); b1 = rng.normal(size=H) * 0.1
+    w2 = rng.normal(scale=0.8, size=(E, H)); b2 = rng.normal(size=E) * 0.1
+    slots = rng.integers(0, E, size=(B, 1)).astype(np.int32)
+    he = rng.normal(size=(B, emb)); ce = rng.normal(size=(B, ctx))
+    d = lambda a: torch.as_tensor(a, device="cuda")
+    probs, demand = kernels.predictor_mlp(d(slots), d(he), d(ce), d(w1), d(b1), d(w2), d(b2),
+                                          want_demand=True, demand_mode="any")
+    p = probs.cpu().numpy()
+    ref = -np.expm1(np.log1p(-p).sum(0))
+    np.testing.assert_allclose(demand.cpu().numpy(), ref, rtol=1e-10, atol=1e-14)
