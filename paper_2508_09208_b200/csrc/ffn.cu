@@ -3,9 +3,7 @@
 // [W_in (N1 x d) | W_out (d x d_ff)], N1 = d_ff (ReLU) or 2*d_ff (SwiGLU with
 // gate/up interleaved in 128-row blocks) — the device image of the
 // reference's flat `Expert.params` (pkg/src/comoe/moe.py:69-74).
-#include <atomic>
 #include <cstdlib>
-#include <mutex>
 
 #include "grouped_gemm_2sm.cuh"
 #include "../../include/comoe_b200.h"
@@ -29,13 +27,13 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const Group
   return check_launch("grouped_gemm_kernel");
 }
 
-template <int kMode, int kStages, int kEpiWarps, bool kWide = false>
+template <int kMode, int kStages, int kEpiWarps>
 static int launch_gemm_2sm_cfg(const CUtensorMap& tw, const CUtensorMap& tx,
                                const CUtensorMap& to, const GroupedGemmParams& p,
                                cudaStream_t stream) {
-  using C = Gemm2Cfg<kStages, kEpiWarps, kWide>;
+  using C = Gemm2Cfg<kStages, kEpiWarps>;
   if (p.gather_rows) {
-    if constexpr (kMode == kEpiRelu && !kWide) {
+    if constexpr (kMode == kEpiRelu) {
       auto kg = grouped_gemm_2sm_kernel<kMode, kStages, kEpiWarps, true>;
       static bool attr_g = false;
       if (!attr_g) {
@@ -51,7 +49,7 @@ static int launch_gemm_2sm_cfg(const CUtensorMap& tw, const CUtensorMap& tx,
     set_error("grouped_gemm: row gather is only supported with the ReLU epilogue");
     return kUnsupportedShape;
   }
-  auto kern = grouped_gemm_2sm_kernel<kMode, kStages, kEpiWarps, false, kWide>;
+  auto kern = grouped_gemm_2sm_kernel<kMode, kStages, kEpiWarps>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kTotal);
@@ -72,12 +70,9 @@ static int launch_gemm_2sm_cfg(const CUtensorMap& tw, const CUtensorMap& tx,
   return check_launch("grouped_gemm_2sm_kernel");
 }
 
-// pipeline config (COMOE_GEMM2_CFG for A/B runs). 256-token tiles: 0 = 5
-// stages x 8 epilogue warps, 1 = 4 x 8, 2 = 6 x 4 (default: deepest
-// pipeline; ragged C2 +3-5% over 0 — the loads are latency-bound, 4 stages
-// lose 7%); 512-token (wide) tiles: 3 = 4 stages x 4 warps, 4 = 3 x 8,
-// 5 = 3 x 4 (correct, but 3-10% slower: a wide tile's epilogue cannot
-// overlap the next tile's MMAs because it occupies all 512 TMEM columns)
+// pipeline config (COMOE_GEMM2_CFG for A/B runs): 0 = 5 stages x 8 epilogue
+// warps, 1 = 4 x 8, 2 = 6 x 4 (default: deepest pipeline; ragged C2 +3-5%
+// over 0 — the loads are latency-bound, 4 stages lose 7%)
 static int gemm2_cfg() {
   static const int c = [] {
     const char* e = std::getenv("COMOE_GEMM2_CFG");
@@ -93,9 +88,6 @@ static int launch_gemm_2sm(const CUtensorMap& tw, const CUtensorMap& tx, const C
   switch (gemm2_cfg()) {
     case 0: return launch_gemm_2sm_cfg<kMode, 5, 8>(tw, tx, to, p, stream);
     case 1: return launch_gemm_2sm_cfg<kMode, 4, 8>(tw, tx, to, p, stream);
-    case 3: return launch_gemm_2sm_cfg<kMode, 4, 4, true>(tw, tx, to, p, stream);
-    case 4: return launch_gemm_2sm_cfg<kMode, 3, 8, true>(tw, tx, to, p, stream);
-    case 5: return launch_gemm_2sm_cfg<kMode, 3, 4, true>(tw, tx, to, p, stream);
     default: return launch_gemm_2sm_cfg<kMode, 6, 4>(tw, tx, to, p, stream);
   }
 }
@@ -106,42 +98,6 @@ static int gemm_debug() {
     return e ? std::atoi(e) : 0;
   }();
   return d;
-}
-
-// Tile-claim counters for the 2-SM kernel's dynamic scheduler: a per-device
-// ring of kSchedSlots zeroed {next, finished} pairs. Each launch takes the
-// next pair; the kernel's last cluster rearms it, so a pair is reusable as
-// soon as its launch retired (launches on one stream are ordered; up to
-// kSchedSlots launches may be in flight concurrently on different streams).
-// Allocated (and zeroed, synchronously) on a device's first GEMM, so capture
-// a CUDA graph only after one eager call, as for the kernel attributes.
-// Opt-in (COMOE_GEMM_DYNAMIC=1): measured at C2 it does not pay — static
-// round-robin is as fast for GEMM2 and 9% faster for GEMM1 (the pair-to-pair
-// tile-id hand-off costs more than the ragged-group imbalance it removes;
-// the kernel is bound by shared L2/smem throughput, not per-pair work).
-constexpr int kSchedSlots = 256;
-static int* sched_counters() {
-  static const bool on = [] {
-    const char* e = std::getenv("COMOE_GEMM_DYNAMIC");
-    return e && e[0] == '1';
-  }();
-  if (!on) return nullptr;
-  static int* ring[64] = {};
-  static std::atomic<unsigned> next[64];
-  static std::mutex mu;
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-  if (!ring[dev]) {
-    std::lock_guard<std::mutex> lock(mu);
-    if (!ring[dev]) {
-      int* buf = nullptr;
-      // 32 ints (128 B) per slot: no two launches share a cache line
-      if (cudaMalloc(&buf, kSchedSlots * 32 * sizeof(int)) != cudaSuccess) return nullptr;
-      if (cudaMemset(buf, 0, kSchedSlots * 32 * sizeof(int)) != cudaSuccess) return nullptr;
-      ring[dev] = buf;
-    }
-  }
-  return ring[dev] + 32 * (next[dev].fetch_add(1) % kSchedSlots);
 }
 
 // Tile order (both kernels): feature-tile major when one group's weight block
@@ -190,14 +146,13 @@ static int grouped_gemm_impl(const void* a, long a_rows, const void* pool, int n
   const void* b = static_cast<const __nv_bfloat16*>(pool) + b_offset;
   GroupedGemmParams p{group_rows, group_row_base, group_slot, G, N, K,
                       reinterpret_cast<__nv_bfloat16*>(out), ldo, row_token, row_prob,
-                      a_gather, gemm_debug(), ft_major(static_cast<long>(N) * K * 2), nullptr};
+                      a_gather, gemm_debug(), ft_major(static_cast<long>(N) * K * 2)};
   int rc;
   // SwiGLU stays on the 1-SM kernel: a 2-SM variant (gate/up rows split into
   // 64-row boxes per SM, up values handed to the gate warps through shared
   // memory) measured 16% slower at the C2 shape and equal at C5
   if (epi_mode != kEpiSwiGLU && !force_1sm()) {
     COMOE_REQUIRE(G <= kMaxGroups2, kBadArg, "grouped_gemm: G=%d > %d", G, kMaxGroups2);
-    p.sched = sched_counters();
     // 2-SM swap-AB kernel: weights = A (128-feature boxes), tokens = B (128-row boxes)
     rc = make_tmap_bf16_3d(&tb, b, n_slots, N, K, slot_stride, 128);
     if (rc) return rc;

@@ -43,9 +43,6 @@ struct GroupedGemmParams {
                           // 16/128 = L2-resident operands (see the producer); 0 in production
   int ft_major;           // tile order inside a group (0: token tile major,
                           // 1: feature tile major — consecutive CTAs share a weight tile)
-  int* sched;             // 2-SM kernel: {next tile, finished clusters} counters for dynamic
-                          // tile claiming (zero on entry, reset to zero by the last cluster);
-                          // nullptr = static round-robin
 };
 
 constexpr int kGemmBM = 128;

@@ -24,28 +24,21 @@ constexpr int k2BN = 256;                    // max tokens per tile
 constexpr int kMaxGroups2 = 1024;
 constexpr int k2MaxThreads = 128 + 32 * 8;
 
-// kStages: smem pipeline depth; kEpiWarps: 4 or 8 epilogue warps (1 or 2
-// per TMEM lane quarter); kWide: token tiles of up to 512 rows computed as
-// two N<=256 MMAs per k-step that share the weight (A) stage, each into
-// its own 256-column TMEM half — one weight pass per 512 routed tokens
-// instead of per 256 (a C2 expert holds ~512 tokens, so a 256-token tiling
-// re-streams every expert's weights 2-3 times, the last time for a ragged
-// tail of a few dozen tokens).
-template <int kStages, int kEpiWarps, bool kWide = false>
+// kStages: smem pipeline depth (32 KB per stage per SM); kEpiWarps: 4 or 8
+// epilogue warps (1 or 2 per TMEM lane quarter). Measured and not kept
+// (K3): 512-token tiles sharing each weight stage between two
+// MMAs, dynamic tile claiming through a cross-CTA tile-id ring, split
+// weight/token rings, and L2 prefetch of weight boxes.
+template <int kStages, int kEpiWarps>
 struct Gemm2Cfg {
   static constexpr int kThreads = 128 + 32 * kEpiWarps;  // w0 TMA, w1 MMA, w2 TMEM, w3 idle
-  static constexpr int kHalves = kWide ? 2 : 1;          // token MMAs (TMEM halves) per tile
-  static constexpr int kTokTile = 256 * kHalves;         // max tokens per tile
   static constexpr int kABytes = 128 * kGemmBK * 2;     // 128 feature rows x 64 K
-  static constexpr int kBHalfBytes = 128 * kGemmBK * 2; // up to 128 token rows x 64 K per MMA
-  static constexpr int kBBytes = kHalves * kBHalfBytes;
+  static constexpr int kBBytes = 128 * kGemmBK * 2;     // up to 128 token rows x 64 K
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTileBytes = kStages * kStageBytes;
   static constexpr int kXposeBytes = 0;                          // (register transpose)
   static constexpr int kStgBytes = kEpiWarps * 2 * 32 * 64;    // per-warp 2 x (32 tok x 32 feat)
-  static constexpr int kSchedDepth = 8;                  // tile-id ring (dynamic scheduling)
-  static constexpr int kCtrlBytes =
-      (2 * kStages + 4 + 2 * kSchedDepth) * 8 + 16 + kSchedDepth * 4 + (kMaxGroups2 + 1) * 4;
+  static constexpr int kCtrlBytes = (2 * kStages + 4) * 8 + 16 + (kMaxGroups2 + 1) * 4;
   static constexpr int kTotal = 1024 + kTileBytes + kXposeBytes + kStgBytes + kCtrlBytes;
   static_assert(kTotal <= 227 * 1024, "shared memory");
 };
@@ -79,78 +72,6 @@ __device__ __forceinline__ void cluster_sync_all() {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
-// shared::cluster address of `local` in CTA `rank` of the cluster
-__device__ __forceinline__ uint32_t mapa_rank(const void* local, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(local)), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void mbar_arrive_release_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAITC_%=:\n\t"
-      "mbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void st_cluster_u32(uint32_t cluster_addr, int v) {
-  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
-}
-
-// Dynamic tile claiming for a persistent CTA pair. The leader's producer
-// thread claims tile ids from a global counter (atomicAdd, in order, so
-// concurrently running pairs still work on neighbouring tiles and share
-// weights/tokens in L2) and publishes the i-th claim into slot i % depth of
-// a tile-id ring held by BOTH CTAs. Consumers — the peer's producer, the
-// MMA thread and every epilogue warp of both CTAs — read claims in the same
-// order and release the slot on the leader's empty barrier. A pair claims
-// its next tile only when it is ready to load it, so the load imbalance of
-// ragged expert groups (round-robin: max/mean 1.08-1.23 at C2) drops to
-// at most one tile.
-struct TileRing {
-  int* tile;            // [depth] local ring
-  uint64_t* full;       // [depth] local, count 1 (the leader's publish)
-  uint64_t* empty;      // [depth] leader's copy counts every consumer of both CTAs
-  int depth;
-  // publish claim i (= t, drawn earlier so the atomic's L2 round trip
-  // overlaps the previous tile's loads)
-  __device__ __forceinline__ void publish(uint32_t i, int t, bool peer_too) const {
-    const int s = static_cast<int>(i % depth);
-    const uint32_t par = (i / depth) & 1;
-    mbar_wait(&empty[s], par ^ 1);
-    tile[s] = t;
-    if (peer_too) {
-      st_cluster_u32(mapa_rank(&tile[s], 1), t);
-      mbar_arrive_release_cluster(mapa_rank(&full[s], 1));
-    }
-    mbar_arrive(&full[s]);
-  }
-  // consumers in the leader CTA: everything is CTA-local (cta-scope
-  // acquire/release); the peer's consumers need cluster scope
-  __device__ __forceinline__ int consume(uint32_t i, bool is_leader) const {
-    const int s = static_cast<int>(i % depth);
-    const uint32_t par = (i / depth) & 1;
-    if (is_leader) {
-      mbar_wait(&full[s], par);
-      const int t = *reinterpret_cast<volatile int*>(&tile[s]);
-      // relaxed: a release here would also order the MMA thread's in-flight
-      // tcgen05 work and drain the tensor pipe at every tile boundary
-      asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s]))
-                   : "memory");
-      return t;
-    }
-    mbar_wait(&full[s], par);
-    asm volatile("fence.acq_rel.cluster;" ::: "memory");  // pairs with the leader's release
-    const int t = *reinterpret_cast<volatile int*>(&tile[s]);
-    mbar_arrive_release_cluster(mapa_rank(&empty[s], 0));
-    return t;
-  }
-};
 __device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, uint32_t bar,
                                                 int32_t x, int32_t y, uint64_t policy) {
   asm volatile(
@@ -195,8 +116,7 @@ __device__ __forceinline__ void umma_commit_2sm_mc(uint64_t* bar) {
       : "memory");
 }
 
-// tiles of a group: ceil(rows/kTokTile) token tiles x (N/256) feature tiles
-template <int kTokTile>
+// tiles of a group: ceil(rows/256) token tiles x (N/256) feature tiles
 __device__ __forceinline__ void build_tile_prefix_2sm(const int* __restrict__ rows, int G,
                                                       int f_tiles, int* prefix) {
   __shared__ int warp_tot2[k2MaxThreads / 32];
@@ -206,7 +126,7 @@ __device__ __forceinline__ void build_tile_prefix_2sm(const int* __restrict__ ro
   const int g0 = tid * per;
   int local = 0;
   for (int i = 0; i < per; ++i)
-    if (g0 + i < G) local += ((__ldg(rows + g0 + i) + kTokTile - 1) / kTokTile) * f_tiles;
+    if (g0 + i < G) local += ((__ldg(rows + g0 + i) + k2BN - 1) / k2BN) * f_tiles;
   int v = local;
   const int lane = tid & 31, w = tid >> 5;
 #pragma unroll
@@ -222,21 +142,17 @@ __device__ __forceinline__ void build_tile_prefix_2sm(const int* __restrict__ ro
     const int g = g0 + i;
     if (g < G) {
       prefix[g] = run;
-      run += ((__ldg(rows + g) + kTokTile - 1) / kTokTile) * f_tiles;
+      run += ((__ldg(rows + g) + k2BN - 1) / k2BN) * f_tiles;
     }
   }
   if (tid == nthreads - 1) prefix[G] = run;
   __syncthreads();
 }
 
-// A tile = (group, feature tile, token tile). Its tokens split into halves of
-// <= 256 (one MMA and one TMEM half each): ntok[j] valid, nmma[j] padded to 16.
 struct Tile2 {
-  int g, ft, tok0, nh;
-  int ntok[2], nmma[2];
+  int g, ft, tok0, ntok, nmma;
 };
 
-template <int kTokTile>
 __device__ __forceinline__ Tile2 decode_tile2(const int* prefix, const GroupedGemmParams& p,
                                               int f_tiles, int tile) {
   Tile2 t;
@@ -245,32 +161,26 @@ __device__ __forceinline__ Tile2 decode_tile2(const int* prefix, const GroupedGe
   const int rows = __ldg(p.group_rows + t.g);
   int tt;
   if (p.ft_major) {  // big weight blocks: neighbouring pairs share a weight tile
-    const int n_tt = (rows + kTokTile - 1) / kTokTile;
+    const int n_tt = (rows + k2BN - 1) / k2BN;
     tt = local % n_tt;
     t.ft = local / n_tt;
   } else {
     tt = local / f_tiles;
     t.ft = local % f_tiles;
   }
-  t.tok0 = tt * kTokTile;
-  const int n = min(kTokTile, rows - t.tok0);
-  t.ntok[0] = min(k2BN, n);
-  t.ntok[1] = n - t.ntok[0];
-  t.nh = t.ntok[1] > 0 ? 2 : 1;
-  t.nmma[0] = (t.ntok[0] + 15) & ~15;
-  t.nmma[1] = (t.ntok[1] + 15) & ~15;
+  t.tok0 = tt * k2BN;
+  t.ntok = min(k2BN, rows - t.tok0);
+  t.nmma = (t.ntok + 15) & ~15;
   return t;
 }
 
-template <int kMode, int k2Stages, int k2EpiWarps, bool kGather = false, bool kWide = false>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k2EpiWarps, kWide>::kThreads, 1)
+template <int kMode, int k2Stages, int k2EpiWarps, bool kGather = false>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k2EpiWarps>::kThreads, 1)
     grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmap_w,
                             const __grid_constant__ CUtensorMap tmap_x,
                             const __grid_constant__ CUtensorMap tmap_out, GroupedGemmParams p) {
   static_assert(kMode != kEpiSwiGLU, "SwiGLU uses the 1-SM kernel");
-  static_assert(!(kGather && kWide), "row gather uses 256-token tiles");
-  using S = Gemm2Cfg<k2Stages, k2EpiWarps, kWide>;
-  constexpr int kTT = S::kTokTile;
+  using S = Gemm2Cfg<k2Stages, k2EpiWarps>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -282,12 +192,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k
   uint64_t* empty_bar = full_bar + k2Stages;
   uint64_t* tfull_bar = empty_bar + k2Stages;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint64_t* sched_full = tempty_bar + 2;
-  uint64_t* sched_empty = sched_full + S::kSchedDepth;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sched_empty + S::kSchedDepth);
-  int* sched_tile = reinterpret_cast<int*>(tmem_slot + 4);
-  int* prefix = sched_tile + S::kSchedDepth;
-  const TileRing ring{sched_tile, sched_full, sched_empty, S::kSchedDepth};
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  int* prefix = reinterpret_cast<int*>(tmem_slot + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -308,11 +214,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k
       mbar_init(&tfull_bar[a], 1);
       mbar_init(&tempty_bar[a], 2 * k2EpiWarps);  // epilogue warps of both CTAs (leader's copy)
     }
-    for (int s = 0; s < S::kSchedDepth; ++s) {
-      mbar_init(&sched_full[s], 1);
-      // leader's MMA thread + peer's producer + epilogue warps of both CTAs
-      mbar_init(&sched_empty[s], 2 + 2 * k2EpiWarps);
-    }
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -323,13 +224,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k
   }
   pdl_wait();     // group tables / token rows come from the preceding kernels
   pdl_trigger();  // persistent grid: the next kernel may launch and wait
-  build_tile_prefix_2sm<kTT>(p.group_rows, p.G, f_tiles, prefix);
+  build_tile_prefix_2sm(p.group_rows, p.G, f_tiles, prefix);
   tc_fence_before();
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int total_tiles = prefix[p.G];
-  const bool dyn = p.sched != nullptr;
 
   if (warp == 0) {
     // ---------------------------------------------- TMA producer (both CTAs)
@@ -339,54 +239,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k
     const uint64_t pol_x = l2_policy_evict_last();
     int stage = 0;
     uint32_t phase = 0;
-    // leader: claims run two ahead of the tile being loaded and are
-    // published one ahead, so neither the atomic's L2 round trip nor the
-    // cross-CTA hand-off to the peer sits on the load path
-    int c_cur = 0, c_nxt = 0, c_nxt2 = 0;
-    if (dyn && leader && lane == 0) {
-      c_cur = atomicAdd(p.sched, 1);
-      ring.publish(0, c_cur, true);
-      if (c_cur < total_tiles) c_nxt = atomicAdd(p.sched, 1);
-    }
-    for (uint32_t i = 0;; ++i) {
-      int tile = cluster + static_cast<int>(i) * n_clusters;
-      if (dyn) {
-        if (lane == 0) {
-          if (leader) {
-            tile = c_cur;
-            if (tile < total_tiles) {
-              ring.publish(i + 1, c_nxt, true);
-              if (c_nxt < total_tiles) c_nxt2 = atomicAdd(p.sched, 1);
-              c_cur = c_nxt;
-              c_nxt = c_nxt2;
-            }
-          } else {
-            tile = ring.consume(i, false);
-          }
-        }
-        tile = __shfl_sync(0xffffffffu, tile, 0);
-      }
-      if (tile >= total_tiles) break;
-      const Tile2 t = decode_tile2<kTT>(prefix, p, f_tiles, tile);
+    for (int tile = cluster; tile < total_tiles; tile += n_clusters) {
+      const Tile2 t = decode_tile2(prefix, p, f_tiles, tile);
       // (dev attribution: debug 16 = every tile loads slot 0 and token row 0,
       // 128 = slot 0 only — L2-resident operands; +27-42% / +17% at C2)
       const int slot = (p.debug & (16 | 128)) ? 0 : __ldg(p.group_slot + t.g);
       const int feat = t.ft * k2BM + static_cast<int>(rank) * 128;
       const int gbase = (p.debug & 16) ? -t.tok0 : __ldg(p.group_row_base + t.g);
-      // this CTA's token rows of MMA j: the rank-th half of its nmma[j] columns
-      const int row0 = gbase + t.tok0 + static_cast<int>(rank) * (t.nmma[0] >> 1);
-      const int row1 = gbase + t.tok0 + k2BN + static_cast<int>(rank) * (t.nmma[1] >> 1);
-      const uint32_t tx = 2 * (S::kABytes + t.nh * S::kBHalfBytes);
+      const int half0 = t.tok0 + static_cast<int>(rank) * (t.nmma >> 1);
       int idx0 = 0, idx1 = 0, idx2 = 0, idx3 = 0;
       if constexpr (kGather) {
         // this lane gathers rows 4*lane .. 4*lane+3 of the CTA's token half
         // (padding rows point at the group's first token; their columns are dropped)
-        const int half0 = t.tok0 + static_cast<int>(rank) * (t.nmma[0] >> 1);
         int rr[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int r = half0 + 4 * lane + i;
-          rr[i] = __ldg(p.gather_rows + gbase + (r < t.tok0 + t.ntok[0] ? r : t.tok0));
+          rr[i] = __ldg(p.gather_rows + gbase + (r < t.tok0 + t.ntok ? r : t.tok0));
         }
         idx0 = rr[0]; idx1 = rr[1]; idx2 = rr[2]; idx3 = rr[3];
       }
@@ -398,15 +267,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k
             if (leader) mbar_arrive(&full_bar[stage]);
             else mbar_arrive_cluster(fb);
           } else {
-            if (leader) mbar_expect_tx(&full_bar[stage], kGather ? 2 * S::kStageBytes : tx);
+            if (leader) mbar_expect_tx(&full_bar[stage], 2 * S::kStageBytes);
             else mbar_arrive_cluster(fb);
             tma_load_3d_2sm(smem_a + stage * S::kABytes, &tmap_w, fb, kb * kGemmBK, feat, slot, pol_w);
-            if constexpr (!kGather) {
-              uint8_t* b = smem_b + stage * S::kBBytes;
-              tma_load_2d_2sm(b, &tmap_x, fb, kb * kGemmBK, row0, pol_x);
-              if (kWide && t.nh == 2)
-                tma_load_2d_2sm(b + S::kBHalfBytes, &tmap_x, fb, kb * kGemmBK, row1, pol_x);
-            }
+            if constexpr (!kGather)
+              tma_load_2d_2sm(smem_b + stage * S::kBBytes, &tmap_x, fb, kb * kGemmBK,
+                              gbase + half0, pol_x);
           }
         }
         if constexpr (kGather) {
@@ -420,45 +286,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k
     }
   } else if (warp == 1) {
     // ---------------------------------------------- MMA issuer (leader CTA only)
-    // TMEM = two 256-column accumulator halves used as a ring: half sequence
-    // number h -> columns (h&1)*256, use count h>>1. A tile takes nh halves.
     if (leader && elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      uint32_t hseq = 0;
-      for (uint32_t i = 0;; ++i) {
-        const int tile = dyn ? ring.consume(i, true) : cluster + static_cast<int>(i) * n_clusters;
-        if (tile >= total_tiles) break;
-        const Tile2 t = decode_tile2<kTT>(prefix, p, f_tiles, tile);
-        const uint32_t idesc0 = umma_idesc_bf16_f32(k2BM, t.nmma[0]);
-        const uint32_t idesc1 = umma_idesc_bf16_f32(k2BM, kWide && t.nh == 2 ? t.nmma[1] : 16);
-        const uint32_t h0 = hseq, h1 = hseq + 1;
-        mbar_wait(&tempty_bar[h0 & 1], ((h0 >> 1) & 1) ^ 1);
-        if (kWide && t.nh == 2) mbar_wait(&tempty_bar[h1 & 1], ((h1 >> 1) & 1) ^ 1);
+      int it = 0;
+      for (int tile = cluster; tile < total_tiles; tile += n_clusters, ++it) {
+        const Tile2 t = decode_tile2(prefix, p, f_tiles, tile);
+        const uint32_t idesc = umma_idesc_bf16_f32(k2BM, t.nmma);
+        const int acc = it & 1;
+        mbar_wait(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d0 = tmem_base + (h0 & 1) * k2BN;
-        const uint32_t d1 = tmem_base + (h1 & 1) * k2BN;
+        const uint32_t d_tmem = tmem_base + acc * k2BN;
         for (int kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           const uint64_t adesc = umma_desc_k_sw128(smem_u32(smem_a + stage * S::kABytes));
-          const uint64_t bdesc0 = umma_desc_k_sw128(smem_u32(smem_b + stage * S::kBBytes));
+          const uint64_t bdesc = umma_desc_k_sw128(smem_u32(smem_b + stage * S::kBBytes));
 #pragma unroll
           for (int k = 0; k < kGemmBK / 16; ++k)
-            umma_bf16_2sm(d0, adesc + 2 * k, bdesc0 + 2 * k, idesc0, (kb | k) != 0);
-          if (kWide && t.nh == 2) {
-            const uint64_t bdesc1 =
-                umma_desc_k_sw128(smem_u32(smem_b + stage * S::kBBytes + S::kBHalfBytes));
-#pragma unroll
-            for (int k = 0; k < kGemmBK / 16; ++k)
-              umma_bf16_2sm(d1, adesc + 2 * k, bdesc1 + 2 * k, idesc1, (kb | k) != 0);
-          }
+            umma_bf16_2sm(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
           umma_commit_2sm_mc(&empty_bar[stage]);
           if (++stage == k2Stages) { stage = 0; phase ^= 1; }
         }
-        umma_commit_2sm_mc(&tfull_bar[h0 & 1]);
-        if (kWide && t.nh == 2) umma_commit_2sm_mc(&tfull_bar[h1 & 1]);
-        hseq += t.nh;
+        umma_commit_2sm_mc(&tfull_bar[acc]);
       }
     }
   } else if (warp >= 4) {
@@ -474,122 +324,105 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k
     const uint32_t sg0 = smem_u32(stg) + ew * (2 * 32 * 64);
     constexpr bool kTmaStore = kMode != kEpiScaleScatter;  // contiguous rows: TMA bulk store
     int nbuf = 0;
-    uint32_t hseq = 0;
-    for (uint32_t i = 0;; ++i) {
-      int tile = cluster + static_cast<int>(i) * n_clusters;
-      if (dyn) {
-        if (lane == 0) tile = ring.consume(i, leader);
-        tile = __shfl_sync(0xffffffffu, tile, 0);
-      }
-      if (tile >= total_tiles) break;
-      const Tile2 t = decode_tile2<kTT>(prefix, p, f_tiles, tile);
+    int it = 0;
+    for (int tile = cluster; tile < total_tiles; tile += n_clusters, ++it) {
+      const Tile2 t = decode_tile2(prefix, p, f_tiles, tile);
+      const int acc = it & 1;
+      const long row_base = static_cast<long>(__ldg(p.group_row_base + t.g)) + t.tok0;
       const long col0 = static_cast<long>(t.ft) * k2BM + rank * 128 + q * 32;
-      for (int j = 0; j < t.nh; ++j, ++hseq) {
-        const int acc = hseq & 1;
-        const int ntok = t.ntok[j];
-        const long row_base = static_cast<long>(__ldg(p.group_row_base + t.g)) + t.tok0 + j * k2BN;
-        mbar_wait(&tfull_bar[acc], (hseq >> 1) & 1);
-        tc_fence_after();
-        const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * k2BN;
-        const int chunks = (t.nmma[j] + 31) >> 5;
-        bool released = false;
-        for (int ci = sub; ci < chunks; ci += kSubs) {
-          const int c = ci * 32;
-          uint32_t v[32];
-          tmem_ld32(t_row + c, v);
-          tmem_ld_wait();
-          if (ci + kSubs >= chunks) {  // this warp's last TMEM read of the half
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(smem_u32(&tempty_bar[acc]) & kPeerMask);
-            released = true;
-          }
-          if (p.debug & 1) continue;  // dev: TMEM read only
-          // epilogue math in the feature-major registers: v[i] = D[feature lane][token c+i]
-          if constexpr (kMode == kEpiRelu) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(fmaxf(__uint_as_float(v[i]), 0.f));
-          } else if constexpr (kMode == kEpiScaleScatter) {
-            const float my_p = (c + lane < ntok) ? __ldg(p.row_prob + row_base + c + lane) : 0.f;
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              v[i] = __float_as_uint(__uint_as_float(v[i]) * __shfl_sync(0xffffffffu, my_p, i));
-          }
-          // register transpose of feature pairs: lanes (2p, 2p+1) hold features
-          // (2p, 2p+1); for each token pair (2i, 2i+1) the even lane keeps token
-          // 2i and the odd lane token 2i+1, one shfl_xor swapping the partner
-          // feature in. Staging = bf16 [32 tokens][32 features], 64-B rows in
-          // the TMA 64-byte swizzle (16-B chunk c at c ^ ((row/2)%4)): the
-          // even/odd lanes land in opposite bank halves -> conflict-free STS.
-          const int odd = lane & 1;
-          const uint32_t pw = static_cast<uint32_t>(lane >> 1);  // feature-pair word 0..15
-          const uint32_t sg = sg0 + nbuf * (32 * 64);
-          if constexpr (kTmaStore) {
-            if (lane == 0) bulk_wait_read<1>();  // this buffer's previous store has read smem
-            __syncwarp();
-          }
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float send = __uint_as_float(odd ? v[2 * i] : v[2 * i + 1]);
-            const float recv = __shfl_xor_sync(0xffffffffu, send, 1);
-            const float lo = odd ? recv : __uint_as_float(v[2 * i]);          // feature 2p
-            const float hi = odd ? __uint_as_float(v[2 * i + 1]) : recv;      // feature 2p+1
-            const uint32_t row = 2 * i + odd;
-            const uint32_t addr = sg + row * 64 + (((pw >> 2) ^ ((row >> 1) & 3)) << 4) + ((pw & 3) << 2);
-            asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(pack_bf16x2(lo, hi)) : "memory");
-          }
-          __syncwarp();
-          bool stored = false;
-          if constexpr (kTmaStore) {
-            // whole chunk valid: one bulk tensor store (debug 4: dev, force st.global)
-            if (c + 32 <= ntok && !(p.debug & 4)) {
-              fence_async_smem();
-              __syncwarp();
-              if (lane == 0) {
-                tma_store_2d(&tmap_out, stg + (sg - smem_u32(stg)), static_cast<int>(col0),
-                             static_cast<int>(row_base + c));
-                bulk_commit();
-              }
-              nbuf ^= 1;
-              stored = true;
-            }
-          }
-          if (!stored) {  // scatter rows or a partial chunk: 16-B stores, 4 lanes per row
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int r = 8 * i + (lane >> 2), jj = lane & 3;
-              const uint4 x = lds128(sg + r * 64 + ((jj ^ ((r >> 1) & 3)) << 4));
-              const int tk = c + r;
-              if (tk < ntok) {
-                long dst;
-                if constexpr (kMode == kEpiScaleScatter) dst = __ldg(p.row_token + row_base + tk);
-                else dst = row_base + tk;
-                st_global_v4(p.out + dst * p.ldo + col0 + jj * 8, x.x, x.y, x.z, x.w);
-              }
-            }
-            __syncwarp();
-          }
-        }
-        if (!released) {  // no chunk for this warp in a narrow half
+      mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * k2BN;
+      const int chunks = (t.nmma + 31) >> 5;
+      bool released = false;
+      for (int ci = sub; ci < chunks; ci += kSubs) {
+        const int c = ci * 32;
+        uint32_t v[32];
+        tmem_ld32(t_row + c, v);
+        tmem_ld_wait();
+        if (ci + kSubs >= chunks) {  // this warp's last TMEM read of the tile
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(smem_u32(&tempty_bar[acc]) & kPeerMask);
+          released = true;
         }
+        if (p.debug & 1) continue;  // dev: TMEM read only
+        // epilogue math in the feature-major registers: v[j] = D[feature lane][token c+j]
+        if constexpr (kMode == kEpiRelu) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(fmaxf(__uint_as_float(v[j]), 0.f));
+        } else if constexpr (kMode == kEpiScaleScatter) {
+          const float my_p = (c + lane < t.ntok) ? __ldg(p.row_prob + row_base + c + lane) : 0.f;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            v[j] = __float_as_uint(__uint_as_float(v[j]) * __shfl_sync(0xffffffffu, my_p, j));
+        }
+        // register transpose of feature pairs: lanes (2p, 2p+1) hold features
+        // (2p, 2p+1); for each token pair (2j, 2j+1) the even lane keeps token
+        // 2j and the odd lane token 2j+1, one shfl_xor swapping the partner
+        // feature in. Staging = bf16 [32 tokens][32 features], 64-B rows in
+        // the TMA 64-byte swizzle (16-B chunk c at c ^ ((row/2)%4)): the
+        // even/odd lanes land in opposite bank halves -> conflict-free STS.
+        const int odd = lane & 1;
+        const uint32_t pw = static_cast<uint32_t>(lane >> 1);  // feature-pair word 0..15
+        const uint32_t sg = sg0 + nbuf * (32 * 64);
+        if constexpr (kTmaStore) {
+          if (lane == 0) bulk_wait_read<1>();  // this buffer's previous store has read smem
+          __syncwarp();
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float send = __uint_as_float(odd ? v[2 * j] : v[2 * j + 1]);
+          const float recv = __shfl_xor_sync(0xffffffffu, send, 1);
+          const float lo = odd ? recv : __uint_as_float(v[2 * j]);          // feature 2p
+          const float hi = odd ? __uint_as_float(v[2 * j + 1]) : recv;      // feature 2p+1
+          const uint32_t row = 2 * j + odd;
+          const uint32_t addr = sg + row * 64 + (((pw >> 2) ^ ((row >> 1) & 3)) << 4) + ((pw & 3) << 2);
+          asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(pack_bf16x2(lo, hi)) : "memory");
+        }
+        __syncwarp();
+        bool stored = false;
+        if constexpr (kTmaStore) {
+          // whole chunk valid: one bulk tensor store (debug 4: dev, force st.global)
+          if (c + 32 <= t.ntok && !(p.debug & 4)) {
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmap_out, stg + (sg - smem_u32(stg)), static_cast<int>(col0),
+                           static_cast<int>(row_base + c));
+              bulk_commit();
+            }
+            nbuf ^= 1;
+            stored = true;
+          }
+        }
+        if (!stored) {  // scatter rows or a partial chunk: 16-B stores, 4 lanes per row
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int r = 8 * i + (lane >> 2), j = lane & 3;
+            const uint4 x = lds128(sg + r * 64 + ((j ^ ((r >> 1) & 3)) << 4));
+            const int tk = c + r;
+            if (tk < t.ntok) {
+              long dst;
+              if constexpr (kMode == kEpiScaleScatter) dst = __ldg(p.row_token + row_base + tk);
+              else dst = row_base + tk;
+              st_global_v4(p.out + dst * p.ldo + col0 + j * 8, x.x, x.y, x.z, x.w);
+            }
+          }
+          __syncwarp();
+        }
+      }
+      if (!released) {  // no chunk for this warp in a narrow tile
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(smem_u32(&tempty_bar[acc]) & kPeerMask);
       }
     }
   }
+
   if (warp >= 4 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   tc_fence_before();
   cluster_sync_all();
-  if (dyn && leader && threadIdx.x == 0) {
-    // every pair has drawn its end-of-work claim before counting itself
-    // finished, so the last one can rearm the counters for the next launch
-    __threadfence();
-    if (atomicAdd(p.sched + 1, 1) == n_clusters - 1) {
-      atomicExch(p.sched, 0);
-      atomicExch(p.sched + 1, 0);
-    }
-  }
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base)

@@ -246,3 +246,24 @@ def test_replayed_trace_routing_matches_oracle():
                 w_in, w_out = O.split_expert(_np(w[group[t, j]]), d, d_ff, "relu")
                 ref[t] += pr[t, j] * O.expert_ffn(xs[t:t + 1], w_in, w_out, "relu")[0]
     assert O.normwise_error(_np(y), ref) < NORMWISE_TOL
+
+
+def test_gather_gemm1_matches_permuted_copy():
+    """The opt-in GEMM1 that gathers token rows with TMA gather4 (index-only
+    permute, a_gather = row_token) computes exactly what the permuted-copy
+    path computes."""
+    from paper_2508_09208_b200 import kernels
+    T, d, d_ff, E = 2048, 256, 512, 8
+    layer, x, wg, w = _build(T, d, d_ff, E, "relu", 1, 1.25)
+    layer.forward(x)
+    r = layer.last
+    ws = layer._workspace(T)
+    h_copy = torch.empty_like(ws["h"])
+    h_gather = torch.empty_like(ws["h"])
+    kernels.grouped_gemm(r.perm.x_perm, layer.pool.data, 0, d_ff, r.scan.group_kept,
+                         r.scan.group_base, layer.group_slot, kernels.EPI_RELU, h_copy)
+    kernels.grouped_gemm(x, layer.pool.data, 0, d_ff, r.scan.group_kept, r.scan.group_base,
+                         layer.group_slot, kernels.EPI_RELU, h_gather, a_gather=r.perm.row_token)
+    torch.cuda.synchronize()
+    rows = int(r.scan.group_kept.sum())
+    assert torch.equal(h_copy[:rows], h_gather[:rows])
