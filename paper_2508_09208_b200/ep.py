@@ -83,13 +83,23 @@ class DeviceOps:
         return perm.x_perm, perm.token_pos
 
     def expert_ffn(self, recv_rows, recv_counts, El, C, world):
+        """Grouped FFN over the receive buffer [src][local expert][C] rows.
+        Groups are enumerated expert-major (j -> local expert j // world,
+        source j % world), so the tiles of one expert's `world` source
+        blocks run on neighbouring CTA pairs and share its weights in L2
+        (source-major order re-streamed each expert's weights once per
+        source)."""
         L = self.layer
         dev = recv_rows.device
         G = world * El
-        base = self._buf(("gbase", G, C),
-                         lambda: torch.arange(G, dtype=torch.int32, device=dev) * C)
-        slot = self._buf(("gslot", G, El),
-                         lambda: (torch.arange(G, dtype=torch.int32, device=dev) % El).contiguous())
+        # buffer block of group j: src * El + le
+        block = self._buf(("gblock", world, El), lambda: (
+            torch.arange(G, device=dev) % world * El + torch.arange(G, device=dev) // world
+        ).to(torch.int64))
+        base = self._buf(("gbase", world, El, C), lambda: (block * C).to(torch.int32))
+        slot = self._buf(("gslot", world, El),
+                         lambda: (torch.arange(G, dtype=torch.int32, device=dev) // world).contiguous())
+        recv_counts = recv_counts.index_select(0, block).contiguous()
         rows = recv_rows.shape[0]
         h = self._buf(("h", rows), lambda: torch.empty((rows, L.d_ff), dtype=torch.bfloat16,
                                                        device=dev))

@@ -66,3 +66,37 @@ def test_expert_parallel_world1_matches_oracle():
     assert (info["pos"] < 0).sum() > 0
     assert O.normwise_error(y.float().cpu().numpy(), ref) < 1e-2
     dist.destroy_process_group()
+
+
+def test_ep_expert_ffn_expert_major_groups_world4():
+    """The receiver-side grouped FFN of expert parallelism with a simulated
+    world of 4 on one GPU: groups enumerated expert-major over the
+    [src][local expert][C] receive buffer must give every block the FFN of
+    its own local expert (fp32 torch reference, bf16 tolerance)."""
+    from paper_2508_09208_b200 import ExpertPool, MoELayer, kernels
+    from paper_2508_09208_b200.ep import DeviceOps
+    world, E, d, d_ff, C = 4, 16, 256, 512, 96
+    El = E // world
+    g = torch.Generator().manual_seed(7)
+    numel = kernels.expert_numel(d, d_ff, kernels.ACT_RELU)
+    w = (torch.randn(El, numel, generator=g) * 0.05).to(torch.bfloat16).cuda()
+    pool = ExpertPool(El, numel)
+    pool.data[:, :numel].copy_(w)
+    wg = (torch.randn(d, E, generator=g) / math.sqrt(d)).cuda()
+    ops = DeviceOps(MoELayer(wg, pool, d_ff, capacity_factor=1.0, expert_slots=[0] * E))
+    recv = torch.randn(world * El * C, d, generator=g).to(torch.bfloat16).cuda()
+    counts = torch.randint(0, C + 1, (world * El,), generator=g, dtype=torch.int32).cuda()
+    y = ops.expert_ffn(recv, counts, El, C, world)
+    torch.cuda.synchronize()
+    for src in range(world):
+        for le in range(El):
+            blk = src * El + le
+            n = int(counts[blk])
+            if n == 0:
+                continue
+            xs = recv[blk * C: blk * C + n].float()
+            wi = w[le, : d_ff * d].view(d_ff, d).float()
+            wo = w[le, d_ff * d: 2 * d_ff * d].view(d, d_ff).float()
+            ref = torch.relu(xs @ wi.t()).to(torch.bfloat16).float() @ wo.t()
+            got = y[blk * C: blk * C + n].float()
+            assert (got - ref).norm() / ref.norm() < 5e-3, (src, le)
