@@ -136,6 +136,20 @@ def test_swiglu_large_experts_feature_major_order():
     assert O.normwise_error(_np(y), ref) < NORMWISE_TOL
 
 
+def test_relu_large_experts_feature_major_order():
+    """2-SM ReLU GEMMs with weight blocks above 32 MB (d 1024, d_ff 16384:
+    33.5 MB) take the feature-tile-major order; outputs must not change."""
+    T, d, d_ff, E = 640, 1024, 16384, 2
+    layer, x, wg, w = _build(T, d, d_ff, E, "relu", 1, 1.25, seed=6)
+    y = layer.forward(x, want_logits=True)
+    torch.cuda.synchronize()
+    logits = layer.last.gate.logits.cpu().numpy()
+    ref, info = O.layer_forward(_np(x), _np(wg), [_np(w[e]) for e in range(E)], top_k=1,
+                                capacity_factor=1.25, act="relu", d_ff=d_ff, logits=logits)
+    _check_routing(layer, x, wg, info, T)
+    assert O.normwise_error(_np(y), ref) < NORMWISE_TOL
+
+
 def test_merged_variant_routing_and_output():
     """8 experts merged into 4 groups: slot remap in the gate, capacity on
     the merged count, FFN on merged pool slots."""
