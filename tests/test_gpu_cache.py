@@ -136,3 +136,65 @@ def test_activate_variant_cache_for_fused_layer():
     torch.cuda.synchronize()
     assert torch.equal(y, y_ref)
     assert cache.prio_threshold <= 1.0 and len(cache.priorities) == len(principals)
+
+
+def test_variant_controller_switches_under_memory_trace():
+    """Live variant switching (simulator.py:624-680): a memory trace drops
+    below the original model's requirement (forced switch to a fused
+    variant) and recovers (hysteresis, then switch back). After every switch
+    the cached layer reproduces the all-resident forward of the active
+    variant bit for bit."""
+    from paper_2508_09208_b200 import ExpertPool, MoELayer, kernels
+    from paper_2508_09208_b200 import aggregation as A
+    from paper_2508_09208_b200.moe import (Expert, MoeModel, MoeModelSpec,
+                                           cosine_only_calibration, stats_from_routing)
+    from paper_2508_09208_b200.switching import VariantController
+    T, d, d_ff, E = 1024, 256, 512, 8
+    g = torch.Generator().manual_seed(31)
+    x = torch.randn(T, d, generator=g).to(torch.bfloat16).cuda()
+    wg = (torch.randn(d, E, generator=g) / math.sqrt(d)).cuda()
+    numel = kernels.expert_numel(d, d_ff, kernels.ACT_RELU)
+    pool = ExpertPool(E + 8, numel)
+    for s in range(E):
+        pool.view(pool.alloc()).copy_((torch.randn(numel, generator=g) * 0.02).to(torch.bfloat16).cuda())
+    ref_layer = MoELayer(wg, pool, d_ff, capacity_factor=1.25)
+    stats = stats_from_routing({1: ref_layer.route(x).gate.expert_idx}, E)
+    eb = float(pool.slot_bytes)
+    spec = MoeModelSpec(1, (1,), (), E, eb, 1, numel)
+    model = MoeModel(spec, {(1, s): Expert(1, s, pool.view(s), eb) for s in range(E)})
+    lib = A.build_library(model, stats, [A.FusionConfig(mode="fixed", r=0.5),
+                                         A.FusionConfig(mode="fixed", r=0.25)],
+                          1.0, cosine_only_calibration(), pool=pool)
+    stores = {}
+    for v in lib.variants:
+        _, principals = v.group_table(1, E)
+        stores[v.variant_id] = {1: torch.stack([v.retained[1][p].params.cpu() for p in principals])
+                                .contiguous().pin_memory()}
+    ctl = VariantController(lib, stats, stores, {1: (wg, d_ff)}, d_ff,
+                            policy=A.SwitchPolicy(lambda_switch=0.5, switch_cost=0.05,
+                                                  t_threshold=2.0),
+                            reeval_interval=2, required_bytes=lambda v: v.expert_bytes,
+                            workspace_slots=1)
+
+    def check():
+        ref_layer.use_variant(ctl.variant, 1)
+        y_ref = ref_layer.forward(x)
+        y = ctl.forward(x, 1)
+        torch.cuda.synchronize()
+        assert torch.equal(y, y_ref), ctl.variant.variant_id
+
+    big = 10 * eb
+    ctl.start(big)
+    assert ctl.variant.perf_estimate == max(v.perf_estimate for v in lib.variants)
+    check()
+    top = ctl.variant.variant_id
+    trace = [big, big, 4.5 * eb, 4.5 * eb, 4.5 * eb, 2.5 * eb, 2.5 * eb, big, big, big, big, big]
+    switches = []
+    for t, m in enumerate(trace, start=1):
+        e = ctl.tick(t, m)
+        if e is not None:
+            switches.append(e)
+            check()
+    assert any(e.forced for e in switches)  # memory dropped below the active variant
+    assert ctl.variant.variant_id == top      # recovered after the hysteresis window
+    assert all(e.migrated_bytes > 0 and e.seconds > 0 for e in switches)
