@@ -43,6 +43,8 @@ def _args():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--force-ep", action="store_true",
+                    help="dev: run the expert-parallel layer (NCCL) even at one GPU")
     return ap.parse_args()
 
 
@@ -153,7 +155,7 @@ def run_reference(args):
     value = tok * args.steps / dt
     sample = (f"{tok} tokens per step of the C2 layer (E=128, cf 1.25 -> C=40), NumPy fp32 BLAS "
               f"oracle port of the layer forward, {threads} host threads")
-    print(json.dumps({
+    _emit({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
@@ -161,7 +163,7 @@ def run_reference(args):
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }), flush=True)
+    })
 
 
 # ---------------------------------------------------------------- GPU arm
@@ -187,8 +189,11 @@ def run_ours(args):
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    if world > 1 or args.force_ep:
+        os.environ.setdefault("NCCL_DEBUG", "WARN")  # stdout carries exactly one JSON line
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29555")
+        dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
 
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if \
         (ROOT / "MEASURED_PEAKS.json").exists() else {}
@@ -198,7 +203,7 @@ def run_ours(args):
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
     x = torch.randn(T_PER_GPU, D, device=dev, generator=g).to(torch.bfloat16)
     wg = torch.randn(D, E, device=dev, generator=torch.Generator(device=dev).manual_seed(1)) / math.sqrt(D)
-    if world > 1:
+    if world > 1 or args.force_ep:
         from paper_2508_09208_b200.ep import EPMoELayer
         layer = EPMoELayer.synthetic(wg, D_FF, E, world, rank, capacity_factor=CF, seed=2)
     else:
@@ -252,16 +257,19 @@ def run_ours(args):
 
     # tokens processed: every token passes the gate and the combine; report kept ratio too
     kept = int(layer.last.scan.group_kept.sum().item()) if hasattr(layer, "last") and layer.last else None
+    if hasattr(layer, "ops") and getattr(layer.ops, "last_recv_counts", None) is not None:
+        kept = int(layer.ops.last_recv_counts.sum().item())  # EP: rows this rank's GEMMs compute
     value = T_PER_GPU * world / (ms * 1e-3)
 
     # dominant kernel roofline: grouped GEMM (ffn1/ffn2) on the tensor pipe
     dom = max(("ffn1", "ffn2"), key=lambda k: stages.get(k, 0.0))
     rows = kept if kept is not None else T_PER_GPU
     flops = 2.0 * rows * D * D_FF
-    achieved = flops / (stages[dom] * 1e-3) / 1e12
+    achieved = flops / (stages[dom] * 1e-3) / 1e12 if stages.get(dom) else None
     prof = _profile_summary() or {}
     roofline = {"bound": "tensor", "kernel": f"grouped_gemm ({dom})", "achieved": achieved,
-                "peak": bf16_peak, "unit": "TFLOP/s", "frac": achieved / bf16_peak,
+                "peak": bf16_peak, "unit": "TFLOP/s",
+                "frac": achieved / bf16_peak if achieved is not None else None,
                 "peak_source": peak_src,
                 "algorithmic": f"2*kept_rows*d*d_ff = {flops:.4g} FLOP per launch (kept_rows={rows})",
                 "traffic": prof.get(f"{dom}_dram_bytes_per_launch")}
@@ -318,13 +326,31 @@ def run_ours(args):
             "gpu_launches": launches, "clocks": clk.summary(),
             "stages_ms": stages, "kept_rows": kept,
         }
-        print(json.dumps(line), flush=True)
-    if world > 1:
+        _emit(line)
+    if dist.is_initialized():
         dist.destroy_process_group()
+
+
+def _claim_stdout():
+    """Stdout carries exactly one JSON line: keep a private handle on the
+    original fd 1 and point fd 1 at stderr, so banners printed by native
+    libraries (NCCL's version line, ptxas warnings) cannot interleave."""
+    global _OUT
+    sys.stdout.flush()
+    _OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+
+
+_OUT = sys.stdout
+
+
+def _emit(obj):
+    print(json.dumps(obj), file=_OUT, flush=True)
 
 
 def main():
     args = _args()
+    _claim_stdout()
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -30,22 +30,37 @@ def ep_capacity(tokens_per_rank: int, n_experts: int, top_k: int, capacity_facto
     return kernels.capacity_for(tokens_per_rank, n_experts, top_k, capacity_factor)
 
 
-def ep_forward(x, ops, world: int, n_experts: int, capacity: int, group=None):
-    """One EP layer forward of this rank's tokens `x` [T_g, d]."""
+class _NoStage:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
+def ep_forward(x, ops, world: int, n_experts: int, capacity: int, group=None, stage=None):
+    """One EP layer forward of this rank's tokens `x` [T_g, d]. `stage`:
+    optional callable(name) -> context manager timing each step (bench.py)."""
+    st = stage if stage is not None else (lambda name: _NoStage())
     E, C = n_experts, capacity
     El = E // world
-    route = ops.route(x)                                # gate + scan (counts per global expert)
-    send_rows, token_pos = ops.dispatch(x, route, C)    # [E*C, d] fixed layout
-    kept = route.kept                                   # [E] int32, rows per expert from me
-    recv_counts = torch.empty_like(kept)
-    dist.all_to_all_single(recv_counts, kept, group=group)
-    recv_rows = torch.empty_like(send_rows)
-    dist.all_to_all_single(recv_rows, send_rows, group=group)
+    with st("route"):
+        route = ops.route(x)                                # gate + scan (counts per global expert)
+    with st("permute"):
+        send_rows, token_pos = ops.dispatch(x, route, C)    # [E*C, d] fixed layout
+    kept = route.kept                                       # [E] int32, rows per expert from me
+    with st("a2a_dispatch"):
+        recv_counts = torch.empty_like(kept)
+        dist.all_to_all_single(recv_counts, kept, group=group)
+        recv_rows = torch.empty_like(send_rows)
+        dist.all_to_all_single(recv_rows, send_rows, group=group)
     # groups on the receiver: (src, local expert) -> rows recv_counts[src*El+le]
-    y_recv = ops.expert_ffn(recv_rows, recv_counts, El, C, world)
-    y_back = torch.empty_like(y_recv)
-    dist.all_to_all_single(y_back, y_recv, group=group)
-    return ops.combine(y_back, token_pos, route)
+    y_recv = ops.expert_ffn(recv_rows, recv_counts, El, C, world, stage=st)
+    with st("a2a_combine"):
+        y_back = torch.empty_like(y_recv)
+        dist.all_to_all_single(y_back, y_recv, group=group)
+    with st("combine"):
+        return ops.combine(y_back, token_pos, route)
 
 
 class DeviceOps:
@@ -82,7 +97,7 @@ class DeviceOps:
         kernels.permute(x, route.gate, fixed, C, rows, y_zero=None, out=perm)
         return perm.x_perm, perm.token_pos
 
-    def expert_ffn(self, recv_rows, recv_counts, El, C, world):
+    def expert_ffn(self, recv_rows, recv_counts, El, C, world, stage=None):
         """Grouped FFN over the receive buffer [src][local expert][C] rows.
         Groups are enumerated expert-major (j -> local expert j // world,
         source j % world), so the tiles of one expert's `world` source
@@ -100,15 +115,19 @@ class DeviceOps:
         slot = self._buf(("gslot", world, El),
                          lambda: (torch.arange(G, dtype=torch.int32, device=dev) // world).contiguous())
         recv_counts = recv_counts.index_select(0, block).contiguous()
+        self.last_recv_counts = recv_counts  # rows this rank computes (bench FLOP count)
         rows = recv_rows.shape[0]
         h = self._buf(("h", rows), lambda: torch.empty((rows, L.d_ff), dtype=torch.bfloat16,
                                                        device=dev))
         y = self._buf(("y", rows), lambda: torch.empty_like(recv_rows))
         n1 = 2 * L.d_ff if L.act == "swiglu" else L.d_ff
-        kernels.grouped_gemm(recv_rows, L.pool.data, 0, n1, recv_counts, base, slot,
-                             kernels.EPI_SWIGLU if L.act == "swiglu" else kernels.EPI_RELU, h)
-        kernels.grouped_gemm(h, L.pool.data, n1 * L.d, L.d, recv_counts, base, slot,
-                             kernels.EPI_STORE, y)
+        st = stage if stage is not None else (lambda name: _NoStage())
+        with st("ffn1"):
+            kernels.grouped_gemm(recv_rows, L.pool.data, 0, n1, recv_counts, base, slot,
+                                 kernels.EPI_SWIGLU if L.act == "swiglu" else kernels.EPI_RELU, h)
+        with st("ffn2"):
+            kernels.grouped_gemm(h, L.pool.data, n1 * L.d, L.d, recv_counts, base, slot,
+                                 kernels.EPI_STORE, y)
         return y
 
     def combine(self, y_back, token_pos, route):
@@ -156,7 +175,7 @@ class EPMoELayer:
 
     def forward(self, x, out=None, timer=None):
         y = ep_forward(x, self.ops, self.world, self.E, self.capacity(x.shape[0]),
-                       group=self.group)
+                       group=self.group, stage=timer)
         if out is not None:
             out.copy_(y)
             return out

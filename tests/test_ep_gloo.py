@@ -54,7 +54,7 @@ class OracleOps:
                     rows[pos[t, j]] = xn[t]
         return torch.from_numpy(rows), pos
 
-    def expert_ffn(self, recv_rows, recv_counts, El, C, world):
+    def expert_ffn(self, recv_rows, recv_counts, El, C, world, stage=None):
         out = torch.zeros_like(recv_rows)
         cnt = recv_counts.numpy()
         for src in range(world):
