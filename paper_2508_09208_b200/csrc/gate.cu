@@ -57,6 +57,7 @@ struct GateParams {
   float* gate_prob;     // [T, k]
   int* local_rank;      // [T, k]
   int* tile_hist;       // [k][ntiles][G]
+  int debug;            // dev attribution (COMOE_GATE_DEBUG): 1 no router loads, 2 x from tile 0, 4 no x loads
 };
 
 // kPair: CTA pair (cta_group::2, M = 256 tokens): each SM stages its own 128
@@ -74,14 +75,100 @@ struct GateSmem {
   static constexpr int kTotal = 1024 + kTileBytes + kCtrlBytes;
 };
 
+// kCat (pair, two terms): the two router terms are one N = 2*EP operand —
+// CTA rank r stages term r for every expert, so D[:, e] = x.hi_e and
+// D[:, EP+e] = x.mid_e and logit_e = D[:, e] + D[:, EP+e] (one fp32 add in
+// the epilogue). One MMA per k-step instead of one per term: the token tile
+// is read from shared memory once, not once per term (the per-term form kept
+// the tensor pipe ~50% busy with the TMA ring full: profiles/r1_ncu_gate_*).
+// Running top-2 of (value, expert id) for ascending ids (strict '>': the
+// lowest id wins ties).
+struct GateTop2 {
+  float v1 = -INFINITY, v2 = -INFINITY;
+  int i1 = -1, i2 = -1;
+  __device__ __forceinline__ void push(float v, int e) {
+    const bool g1 = v > v1, g2 = v > v2;
+    v2 = g1 ? v1 : (g2 ? v : v2);
+    i2 = g1 ? i1 : (g2 ? e : i2);
+    v1 = g1 ? v : v1;
+    i1 = g1 ? e : i1;
+  }
+};
+// (va, ia) ranks before (vb, ib): larger value, then lower id; an empty entry
+// (id -1) ranks last.
+__device__ __forceinline__ bool gate_before(float va, int ia, float vb, int ib) {
+  return va > vb || (va == vb && static_cast<unsigned>(ia) < static_cast<unsigned>(ib));
+}
+__device__ __forceinline__ void gate_top2_merge(const GateTop2& a, const GateTop2& b, float& v1,
+                                                int& i1, float& v2, int& i2) {
+  if (gate_before(a.v1, a.i1, b.v1, b.i1)) {
+    v1 = a.v1; i1 = a.i1;
+    const bool x = gate_before(a.v2, a.i2, b.v1, b.i1);
+    v2 = x ? a.v2 : b.v1; i2 = x ? a.i2 : b.i1;
+  } else {
+    v1 = b.v1; i1 = b.i1;
+    const bool x = gate_before(a.v1, a.i1, b.v2, b.i2);
+    v2 = x ? a.v1 : b.v2; i2 = x ? a.i1 : b.i2;
+  }
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// Chunk loads for the pipelined epilogue: 16 columns (plus the 16 mid-term
+// columns EP further with kCat) issued without waiting; gate_ld_wait names
+// the destination registers so the compiler cannot read them before the wait.
+template <bool kCat, int EP>
+__device__ __forceinline__ void gate_ld_chunk(uint32_t col, uint32_t (&r)[kCat ? 32 : 16]) {
+  tmem_ld16(col, *reinterpret_cast<uint32_t(*)[16]>(&r[0]));
+  if constexpr (kCat) tmem_ld16(col + EP, *reinterpret_cast<uint32_t(*)[16]>(&r[16]));
+}
+template <bool kCat>
+__device__ __forceinline__ void gate_ld_wait(uint32_t (&r)[kCat ? 32 : 16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]),
+                 "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]),
+                 "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
+               :
+               : "memory");
+  if constexpr (kCat)
+    asm volatile(""
+                 : "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),
+                   "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]),
+                   "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+                 :
+                 : "memory");
+}
+
+// 16 logits of this thread's token starting at TMEM column `col`; with kCat
+// the hi and mid partial logits sit EP columns apart and are summed here.
+template <bool kCat, int EP>
+__device__ __forceinline__ void gate_logits16(uint32_t col, uint32_t (&r)[16]) {
+  tmem_ld16(col, r);
+  if constexpr (kCat) {
+    uint32_t m[16];
+    tmem_ld16(col + EP, m);
+    tmem_ld_wait();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) + __uint_as_float(m[j]));
+  } else {
+    tmem_ld_wait();
+  }
+}
+
 template <int EP, int kStages, bool kPair, int kTerms>
 __global__ void __launch_bounds__(kGateThreads, 1)
     gate_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 const __grid_constant__ CUtensorMap tmap_w, GateParams p) {
   using S = GateSmem<EP, kStages, kPair, kTerms>;
-  constexpr uint32_t kTmemCols = 2 * EP <= 32 ? 32 : (2 * EP <= 64 ? 64 : (2 * EP <= 128 ? 128 : 256));
-  constexpr uint32_t kIdesc = umma_idesc_bf16_f32(kPair ? 256 : kGemmBM, EP);
+  constexpr bool kCat = kPair && kTerms == 2;
+  constexpr int kAccCols = kCat ? 2 * EP : EP;  // TMEM columns of one accumulator
+  constexpr uint32_t kTmemCols =
+      2 * kAccCols <= 32 ? 32 : (2 * kAccCols <= 64 ? 64 : (2 * kAccCols <= 128 ? 128 : (2 * kAccCols <= 256 ? 256 : 512)));
+  constexpr uint32_t kIdesc = umma_idesc_bf16_f32(kPair ? 256 : kGemmBM, kAccCols);
   constexpr int kBRows = S::kBRows;
+  if (p.debug & 32) return;  // dev: empty launch
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -141,7 +228,8 @@ __global__ void __launch_bounds__(kGateThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0) {
+  if (p.debug & 64) {  // dev: prologue + epilogue of the kernel only
+  } else if (warp == 0) {
     if (elect_one()) {
       // keep x in L2: the permute re-reads every row right after the gate
       const uint64_t pol_x = l2_policy_evict_last();
@@ -155,14 +243,22 @@ __global__ void __launch_bounds__(kGateThreads, 1)
           uint8_t* b = smem_b + stage * S::kBBytes;
           if constexpr (kPair) {
             const uint32_t fb = smem_u32(&full_bar[stage]) & kPeerMask;
-            if (leader) mbar_expect_tx(&full_bar[stage], 2 * S::kStageBytes);
+            const int dbg = p.debug;
+            if (leader)
+              mbar_expect_tx(&full_bar[stage], 2 * ((dbg & 4 ? 0 : S::kABytes) + (dbg & 1 ? 0 : S::kBBytes)));
             else mbar_arrive_cluster(fb);
-            tma_load_2d_2sm(smem_a + stage * S::kABytes, &tmap_x, fb, kb * kGemmBK,
-                            tile * kGemmBM, pol_x);
+            if (!(dbg & 4))
+              tma_load_2d_2sm(smem_a + stage * S::kABytes, &tmap_x, fb, kb * kGemmBK,
+                              (dbg & 2 ? static_cast<int>(rank) : tile) * kGemmBM, pol_x);
+            if constexpr (kCat) {
+              if (!(dbg & 1))
+                tma_load_2d_2sm(b, &tmap_w, fb, kb * kGemmBK, static_cast<int>(rank) * EP, pol_w);
+            } else {
 #pragma unroll
-            for (int term = 0; term < kTerms; ++term)
-              tma_load_2d_2sm(b + term * kBRows * 128, &tmap_w, fb, kb * kGemmBK,
-                              term * EP + static_cast<int>(rank) * kBRows, pol_w);
+              for (int term = 0; term < kTerms; ++term)
+                tma_load_2d_2sm(b + term * kBRows * 128, &tmap_w, fb, kb * kGemmBK,
+                                term * EP + static_cast<int>(rank) * kBRows, pol_w);
+            }
           } else {
             mbar_expect_tx(&full_bar[stage], S::kStageBytes);
             tma_load_2d_hint(smem_a + stage * S::kABytes, &tmap_x, &full_bar[stage], kb * kGemmBK,
@@ -184,17 +280,18 @@ __global__ void __launch_bounds__(kGateThreads, 1)
         const int acc = it & 1;
         mbar_wait(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * EP;
+        const uint32_t d_tmem = tmem_base + acc * kAccCols;
         for (int kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           const uint64_t adesc = umma_desc_k_sw128(smem_u32(smem_a + stage * S::kABytes));
 #pragma unroll
-          for (int term = 0; term < kTerms; ++term) {
+          for (int term = 0; term < (kCat ? 1 : kTerms); ++term) {
             const uint64_t bdesc =
                 umma_desc_k_sw128(smem_u32(smem_b + stage * S::kBBytes + term * kBRows * 128));
 #pragma unroll
             for (int k = 0; k < kGemmBK / 16; ++k) {
+              if (p.debug & 16) continue;  // dev: no MMAs
               if constexpr (kPair)
                 umma_bf16_2sm(d_tmem, adesc + 2 * k, bdesc + 2 * k, kIdesc, (kb | k | term) != 0);
               else
@@ -224,61 +321,80 @@ __global__ void __launch_bounds__(kGateThreads, 1)
       const bool valid = tile_ok && t < p.T;
       mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
       tc_fence_after();
-      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * EP;
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * kAccCols;
 
-      // pass 1: running top-2 over this token's logits (branch-free selects;
-      // strict '>' while scanning ascending expert ids keeps the lowest id on ties)
-      float v1 = -INFINITY, v2 = -INFINITY;
-      int i1 = -1, i2 = -1;
+      // One pass over this token's logits, 16 columns per chunk, the TMEM
+      // load of chunk c+1 in flight while chunk c is reduced; the accumulator
+      // is released right after the last load. Two interleaved top-2 trackers
+      // (even / odd columns; strict '>' in ascending expert order keeps the
+      // lowest id on ties, and the final merge breaks ties by id) and an
+      // online softmax denominator s = sum_e 2^((v_e - m) log2 e), rescaled
+      // when the running max m moves (once per chunk).
+      if (p.debug & 8) {  // dev: no epilogue work
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (kPair) mbar_arrive_cluster(smem_u32(&tempty_bar[acc]) & kPeerMask);
+          else mbar_arrive(&tempty_bar[acc]);
+        }
+        continue;
+      }
+      GateTop2 ta, tb;
+      const bool need_sum = !p.norm_topk;
+      constexpr float kLog2e = 1.4426950408889634f;
+      float m = -INFINITY, s4[2] = {0.f, 0.f};
       float* lrow = (p.logits && valid) ? p.logits + static_cast<long>(t) * p.E : nullptr;
-#pragma unroll 1
-      for (int c = 0; c < EP; c += 16) {
-        uint32_t r[16];
-        tmem_ld16(t_row + c, r);
-        tmem_ld_wait();
+      constexpr int kChunks = EP / 16;
+      uint32_t buf[2][kCat ? 32 : 16];
+      gate_ld_chunk<kCat, EP>(t_row, buf[0]);
+#pragma unroll
+      for (int c = 0; c < kChunks; ++c) {
+        uint32_t(&cur)[kCat ? 32 : 16] = buf[c & 1];
+        gate_ld_wait<kCat>(cur);
+        if (c + 1 < kChunks) {
+          gate_ld_chunk<kCat, EP>(t_row + (c + 1) * 16, buf[(c + 1) & 1]);
+        } else {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (kPair) mbar_arrive_cluster(smem_u32(&tempty_bar[acc]) & kPeerMask);
+            else mbar_arrive(&tempty_bar[acc]);
+          }
+        }
+        float v[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          const int e = c + j;
-          const float v = e < p.E ? __uint_as_float(r[j]) : -INFINITY;
-          const bool g1 = v > v1, g2 = v > v2;
-          v2 = g1 ? v1 : (g2 ? v : v2);
-          i2 = g1 ? i1 : (g2 ? e : i2);
-          v1 = g1 ? v : v1;
-          i1 = g1 ? e : i1;
+          const int e = c * 16 + j;
+          float x = __uint_as_float(cur[j]);
+          if constexpr (kCat) x += __uint_as_float(cur[16 + j]);
+          v[j] = e < p.E ? x : -INFINITY;
+        }
+#pragma unroll
+        for (int j = 0; j < 16; j += 2) {
+          ta.push(v[j], c * 16 + j);
+          tb.push(v[j + 1], c * 16 + j + 1);
         }
         if (lrow) {
 #pragma unroll
           for (int j = 0; j < 16; ++j)
-            if (c + j < p.E) lrow[c + j] = __uint_as_float(r[j]);
+            if (c * 16 + j < p.E) lrow[c * 16 + j] = v[j];
         }
-      }
-      // pass 2 (only when a probability needs the full softmax denominator):
-      // s = sum_e exp(v_e - max), four independent partial sums for ILP
-      float s = 1.f;
-      const bool need_sum = !p.norm_topk;
-      if (need_sum) {
-        constexpr float kLog2e = 1.4426950408889634f;
-        const float mb = v1 * kLog2e;
-        float s4[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 1
-        for (int c = 0; c < EP; c += 16) {
-          uint32_t r[16];
-          tmem_ld16(t_row + c, r);
-          tmem_ld_wait();
+        if (need_sum) {
+          const float mn = fmaxf(m, fmaxf(ta.v1, tb.v1));
+          const float mb = mn * kLog2e;
+          const float sc = m == -INFINITY ? 0.f : ex2_approx((m - mn) * kLog2e);
+          s4[0] *= sc;
+          s4[1] *= sc;
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const float v = __uint_as_float(r[j]);
-            s4[j & 3] += (c + j < p.E) ? exp2f(fmaf(v, kLog2e, -mb)) : 0.f;
-          }
+          for (int j = 0; j < 16; ++j)
+            s4[j & 1] += ex2_approx(fmaf(v[j], kLog2e, -mb));
+          m = mn;
         }
-        s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if constexpr (kPair) mbar_arrive_cluster(smem_u32(&tempty_bar[acc]) & kPeerMask);
-        else mbar_arrive(&tempty_bar[acc]);
-      }
+      float v1, v2;
+      int i1, i2;
+      gate_top2_merge(ta, tb, v1, i1, v2, i2);
+      const float s = need_sum ? s4[0] + s4[1] : 1.f;
 
       // probabilities, slot remap, top-2 fold (all in registers)
       float pr0, pr1 = 0.f;
@@ -363,10 +479,9 @@ __global__ void __launch_bounds__(kGateThreads, 1)
   }
 }
 
-template <int EP, bool kPair, int kTerms>
-static int launch_gate_terms(const CUtensorMap& tx, const CUtensorMap& tw, const GateParams& p,
-                             cudaStream_t stream) {
-  constexpr int kStages = kTerms == 2 ? (kPair ? 5 : 4) : (kPair ? 4 : (EP >= 128 ? 3 : 4));
+template <int EP, bool kPair, int kTerms, int kStages>
+static int launch_gate_stages(const CUtensorMap& tx, const CUtensorMap& tw, const GateParams& p,
+                              cudaStream_t stream) {
   using S = GateSmem<EP, kStages, kPair, kTerms>;
   static_assert(S::kTotal <= 227 * 1024, "gate shared memory");
   auto kern = gate_kernel<EP, kStages, kPair, kTerms>;
@@ -407,6 +522,22 @@ static int launch_gate_terms(const CUtensorMap& tx, const CUtensorMap& tw, const
     cfg.numAttrs = pdl_attr(&attrs[0]);
     cudaLaunchKernelEx(&cfg, kern, tx, tw, p);
     return check_launch("gate_kernel");
+  }
+}
+
+template <int EP, bool kPair, int kTerms>
+static int launch_gate_terms(const CUtensorMap& tx, const CUtensorMap& tw, const GateParams& p,
+                             cudaStream_t stream) {
+  if constexpr (kPair && kTerms == 2) {
+    static const bool six = [] {
+      const char* e = std::getenv("COMOE_GATE_STAGES");
+      return e && e[0] == '6';
+    }();
+    return six ? launch_gate_stages<EP, kPair, kTerms, 6>(tx, tw, p, stream)
+               : launch_gate_stages<EP, kPair, kTerms, 5>(tx, tw, p, stream);
+  } else {
+    constexpr int kStages = kTerms == 2 ? 4 : (kPair ? 4 : (EP >= 128 ? 3 : 4));
+    return launch_gate_stages<EP, kPair, kTerms, kStages>(tx, tw, p, stream);
   }
 }
 
@@ -698,10 +829,16 @@ int comoe_gate_topk(const void* x, int T, int d, const void* wg_split, int E, in
   CUtensorMap tx, tw;
   int rc = make_tmap_bf16_2d(&tx, x, T, d, kGemmBM);
   if (rc) return rc;
-  rc = make_tmap_bf16_2d(&tw, wg_split, 3ull * EP, d, pair ? EP / 2 : EP);
+  // box rows: a whole term per CTA for the concatenated-terms pair kernel
+  rc = make_tmap_bf16_2d(&tw, wg_split, 3ull * EP, d, pair ? (gate_terms() == 2 ? EP : EP / 2) : EP);
   if (rc) return rc;
   GateParams p{T, d, E, top_k, norm_topk, n_groups, (T + kGemmBM - 1) / kGemmBM, slot_map,
-               logits_out, expert_idx, group_idx, gate_prob, local_rank, tile_hist};
+               logits_out, expert_idx, group_idx, gate_prob, local_rank, tile_hist, 0};
+  static const int dbg = [] {
+    const char* e = std::getenv("COMOE_GATE_DEBUG");
+    return e ? std::atoi(e) : 0;
+  }();
+  p.debug = dbg;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   switch (EP) {
     case 16: return pair ? launch_gate<16, true>(tx, tw, p, s) : launch_gate<16, false>(tx, tw, p, s);

@@ -42,6 +42,9 @@ def timed(fn, reps=REPS):
     ts = []
     for _ in range(reps):
         _flush.fill_(1)
+        # keep the GPU busy while the host prepares the launch, so the events
+        # bracket device time only (no host gap before the kernel starts)
+        torch.cuda._sleep(400_000)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         fn()
