@@ -139,6 +139,36 @@ int comoe_grouped_ffn(const void* x_perm, long total_rows, int d, int d_ff, int 
 int comoe_combine(const void* y_perm, const int* token_pos, const float* gate_prob, int T, int d,
                   int top_k, void* y, void* stream);
 
+/* ------------------------------------------------ EP over NVLink peer memory
+ * Replaces the two ncclAllToAll of the EP layer (ep.py ep_forward; the
+ * reference has no EP at all — SURVEY §8e/§8f rank 1). Every rank maps its
+ * peers' receive / output / count / pad buffers through CUDA IPC; the send
+ * layout row r = (dst * El + le) * C + slot lives at row
+ * src * block_rows + r % block_rows of rank dst's buffer
+ * (block_rows = El * C). All calls are stream-ordered and never allocate. */
+int comoe_permute_peers(const void* x, int T, int d, int top_k, const int* group_idx,
+                        const float* gate_prob, const int* local_rank, const int* tile_offset,
+                        const int* group_base, int n_groups, int capacity,
+                        void* const* peer_rows, int n_peers, long block_rows, int src_rank,
+                        int* row_token, float* row_prob, int* token_pos, void* stream);
+int comoe_combine_peers(const void* const* peer_rows, int n_peers, long block_rows, int src_rank,
+                        const int* token_pos, const float* gate_prob, int T, int d, int top_k,
+                        void* y, void* stream);
+/* counts[E] (rows of global expert e from src_rank) -> peer_counts[e / El][src_rank * El + e % El] */
+int comoe_peer_scatter_counts(const int* counts, int E, int world, int src_rank,
+                              int* const* peer_counts, void* stream);
+/* flag barrier: publish epoch (> 0, increasing) into every peer's pad slot
+ * [rank], wait for every peer's epoch in mine; on timeout *err = 1 + peer
+ * (the kernel returns instead of hanging). pads: device array of world
+ * pointers to int[world] pads. */
+int comoe_peer_barrier(int* const* pads, int world, int rank, int epoch, long long timeout_ns,
+                       int* err, void* stream);
+int comoe_ipc_handle_size(void);
+/* handle of the allocation holding ptr, and ptr's offset inside it */
+int comoe_ipc_get_handle(const void* ptr, void* handle_out, long* offset_out);
+int comoe_ipc_open(const void* handle, long offset, void** ptr_out);
+int comoe_ipc_close(void* ptr, long offset);
+
 /* ---------------------------------------------------------------- K5 merge
  * merge_group (pkg/src/comoe/aggregation.py:200-215) for n_groups groups in
  * one launch: out[g] = (sum_{j in g} weights[j] * member[j]) / divisor[g].

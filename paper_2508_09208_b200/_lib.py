@@ -38,6 +38,15 @@ _SIGNATURES = {
     "comoe_grouped_ffn": [_p, _c_long, _c_int, _c_int, _c_int, _p, _c_int, _c_long, _p, _p,
                           _p, _c_int, _p, _p, _c_int, _p, _p, _p],
     "comoe_combine": [_p, _p, _p, _c_int, _c_int, _c_int, _p, _p],
+    "comoe_permute_peers": [_p, _c_int, _c_int, _c_int, _p, _p, _p, _p, _p, _c_int, _c_int, _p,
+                            _c_int, _c_long, _c_int, _p, _p, _p, _p],
+    "comoe_combine_peers": [_p, _c_int, _c_long, _c_int, _p, _p, _c_int, _c_int, _c_int, _p, _p],
+    "comoe_peer_scatter_counts": [_p, _c_int, _c_int, _c_int, _p, _p],
+    "comoe_peer_barrier": [_p, _c_int, _c_int, _c_int, ctypes.c_longlong, _p, _p],
+    "comoe_ipc_handle_size": [],
+    "comoe_ipc_get_handle": [_p, _p, _p],
+    "comoe_ipc_open": [_p, _c_long, _p],
+    "comoe_ipc_close": [_p, _c_long],
     "comoe_merge": [_c_int, _p, _p, _p, _p, _p, _c_int, _c_int, _c_long, _p],
     "comoe_sim_workspace_bytes": [_c_int, _c_int, _c_int, _c_long],
     "comoe_sim_contract": [_c_int, _p, _c_int, _c_long, _p, _c_int, _p, _c_int, _p, _p, _p,
@@ -48,6 +57,7 @@ _SIGNATURES = {
                             _p, _c_int, _p, _p, _c_int, _p, _p],
 }
 _RESTYPES = {"comoe_last_error": ctypes.c_char_p, "comoe_sim_workspace_bytes": _c_long,
+             "comoe_ipc_handle_size": _c_int,
              "comoe_predictor_workspace_bytes": _c_long}
 
 EXPORTED = tuple(_SIGNATURES)

@@ -26,7 +26,7 @@ NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--expt-relaxed-constexpr",
               "-I", str(ROOT / "include")]
 
 SOURCES = ["capi.cu", "gate.cu", "permute.cu", "ffn.cu", "merge.cu",
-           "similarity.cu", "predictor.cu"]
+           "similarity.cu", "predictor.cu", "peer.cu"]
 
 
 def nvcc() -> str:

@@ -10,6 +10,11 @@ Per rank (T_g tokens, E experts, E_l = E / world local experts):
   -> grouped FFN over (source rank, local expert) groups of the receive buffer
   -> all_to_all(rows back) -> combine (token_pos addresses the fixed layout).
 
+`ep_forward_peers` is the same schedule over NVLink peer memory: the permute
+stores rows straight into the owners' receive buffers and the combine loads
+the outputs from the owners' output buffers (CUDA IPC mappings, flag
+barriers; `EPMoELayer(transport="peer")` or COMOE_EP_TRANSPORT=peer).
+
 The collective schedule lives in `ep_forward`, written once against an `ops`
 object: `DeviceOps` calls the sm_100a kernels; tests pass a CPU double so the
 N>1 data movement is exercised with gloo on a CPU-only box. Capacity is per
@@ -18,6 +23,8 @@ forward over rank r's tokens.
 """
 
 from __future__ import annotations
+
+import os
 
 import torch
 import torch.distributed as dist
@@ -63,6 +70,107 @@ def ep_forward(x, ops, world: int, n_experts: int, capacity: int, group=None, st
         return ops.combine(y_back, token_pos, route)
 
 
+class PeerBuffers:
+    """This rank's expert-parallel exchange buffers in HBM and the world's
+    addresses of them (the peer-memory transport, include/comoe_b200.h "EP
+    over NVLink peer memory").
+
+    recv [E*C, d]: rows sent to my experts, laid out [src][local expert][C];
+    y [E*C, d]: my experts' outputs in the same layout, read by the sources;
+    counts [E]: rows received per (src, local expert); pad [world]: barrier
+    flags. Peers' buffers are mapped with CUDA IPC (handles exchanged over
+    `group` with all_gather_object), or — `simulated` — are buffers of other
+    PeerBuffers in this process (a world on one GPU, for tests)."""
+
+    def __init__(self, rows: int, d: int, E: int, world: int, rank: int, device, group=None,
+                 exchange: bool = True):
+        self.rows, self.d, self.E, self.world, self.rank = rows, d, E, world, rank
+        self.block_rows = rows // world
+        self.device = device
+        self.recv = torch.zeros((rows, d), dtype=torch.bfloat16, device=device)
+        self.y = torch.zeros_like(self.recv)
+        self.counts = torch.zeros(E, dtype=torch.int32, device=device)
+        self.pad = torch.zeros(world, dtype=torch.int32, device=device)
+        self.err = torch.zeros(1, dtype=torch.int32, device=device)
+        self.epoch = 0
+        self._opened = []
+        if exchange:
+            self._link_ipc(group)
+
+    _FIELDS = ("recv", "y", "counts", "pad")
+
+    def _link(self, addrs):
+        """addrs[field] = world addresses -> int64 device pointer tables."""
+        for f in self._FIELDS:
+            setattr(self, f + "_ptrs", torch.tensor(addrs[f], dtype=torch.int64, device=self.device))
+
+    def _link_ipc(self, group):
+        mine = {f: kernels.ipc_handle(getattr(self, f)) for f in self._FIELDS}
+        if self.world == 1:
+            allh = [mine]
+        else:
+            allh = [None] * self.world
+            dist.all_gather_object(allh, mine, group=group)
+        addrs = {f: [] for f in self._FIELDS}
+        for q in range(self.world):
+            for f in self._FIELDS:
+                if q == self.rank:
+                    addrs[f].append(getattr(self, f).data_ptr())
+                else:
+                    h, off = allh[q][f]
+                    ptr = kernels.ipc_open(h, off)
+                    self._opened.append((ptr, off))
+                    addrs[f].append(ptr)
+        self._link(addrs)
+
+    @classmethod
+    def simulated(cls, world: int, rows: int, d: int, E: int, device):
+        bufs = [cls(rows, d, E, world, r, device, exchange=False) for r in range(world)]
+        addrs = {f: [getattr(b, f).data_ptr() for b in bufs] for f in cls._FIELDS}
+        for b in bufs:
+            b._link(addrs)
+        return bufs
+
+    def barrier(self, timeout_s: float = 10.0):
+        """Stream-ordered: every later op on this stream runs after every
+        rank's earlier ops (their peer stores included) have completed."""
+        self.epoch += 1
+        kernels.peer_barrier(self.pad_ptrs, self.world, self.rank, self.epoch, self.err, timeout_s)
+
+    def check(self):
+        """Raise if a barrier timed out (synchronises)."""
+        e = int(self.err.item())
+        if e:
+            raise RuntimeError(f"peer barrier: rank {e - 1} did not arrive (epoch {self.epoch})")
+
+    def close(self):
+        for ptr, off in self._opened:
+            kernels.ipc_close(ptr, off)
+        self._opened = []
+
+
+def ep_forward_peers(x, ops, bufs: PeerBuffers, n_experts: int, capacity: int, stage=None):
+    """ep_forward with the all-to-alls replaced by peer-memory stores and
+    loads: permute into the owners' receive buffers (+ counts), barrier,
+    grouped FFN into my output buffer, barrier, combine from the owners'
+    output buffers. Two barriers per forward suffice: a rank reaches the
+    next forward's first barrier only after its combine, and peers write my
+    receive buffer only after the barrier that follows my GEMMs."""
+    st = stage if stage is not None else (lambda name: _NoStage())
+    El = n_experts // bufs.world
+    with st("route"):
+        route = ops.route(x)
+    with st("permute"):
+        token_pos = ops.dispatch_peers(x, route, capacity, bufs)
+    with st("a2a_dispatch"):
+        bufs.barrier()
+    ops.expert_ffn(bufs.recv, bufs.counts, El, capacity, bufs.world, stage=st, y_out=bufs.y)
+    with st("a2a_combine"):
+        bufs.barrier()
+    with st("combine"):
+        return ops.combine_peers(token_pos, route, bufs)
+
+
 class DeviceOps:
     """ep_forward ops backed by the CUDA kernels; owns the EP buffers."""
 
@@ -97,7 +205,32 @@ class DeviceOps:
         kernels.permute(x, route.gate, fixed, C, rows, y_zero=None, out=perm)
         return perm.x_perm, perm.token_pos
 
-    def expert_ffn(self, recv_rows, recv_counts, El, C, world, stage=None):
+    def dispatch_peers(self, x, route, C, bufs):
+        """Permute straight into the owners' receive buffers and scatter the
+        per-expert row counts; returns token_pos (send-layout rows)."""
+        L = self.layer
+        dev, T, E = x.device, x.shape[0], L.E
+        rows = E * C
+        if rows != bufs.rows:
+            raise ValueError(f"peer buffers hold {bufs.rows} rows, this batch needs {rows}")
+        base = self._buf(("base", E, C),
+                         lambda: torch.arange(E, dtype=torch.int32, device=dev) * C)
+        perm = self._buf(("perm_peers", T, rows), lambda: kernels.PermuteOutput(
+            None, torch.empty(rows, dtype=torch.int32, device=dev),
+            torch.empty(rows, dtype=torch.float32, device=dev),
+            torch.empty((T, L.top_k), dtype=torch.int32, device=dev)))
+        fixed = kernels.ScanOutput(route.scan.tile_offset, route.scan.group_count,
+                                   route.scan.group_kept, base)
+        kernels.permute_peers(x, route.gate, fixed, C, bufs.recv_ptrs, bufs.block_rows,
+                              bufs.rank, out=perm)
+        kernels.peer_scatter_counts(route.kept, bufs.world, bufs.rank, bufs.counts_ptrs)
+        return perm.token_pos
+
+    def combine_peers(self, token_pos, route, bufs):
+        return kernels.combine_peers(bufs.y_ptrs, bufs.block_rows, bufs.rank, token_pos,
+                                     route.gate.gate_prob, bufs.d)
+
+    def expert_ffn(self, recv_rows, recv_counts, El, C, world, stage=None, y_out=None):
         """Grouped FFN over the receive buffer [src][local expert][C] rows.
         Groups are enumerated expert-major (j -> local expert j // world,
         source j % world), so the tiles of one expert's `world` source
@@ -119,7 +252,8 @@ class DeviceOps:
         rows = recv_rows.shape[0]
         h = self._buf(("h", rows), lambda: torch.empty((rows, L.d_ff), dtype=torch.bfloat16,
                                                        device=dev))
-        y = self._buf(("y", rows), lambda: torch.empty_like(recv_rows))
+        y = y_out if y_out is not None else self._buf(("y", rows),
+                                                       lambda: torch.empty_like(recv_rows))
         n1 = 2 * L.d_ff if L.act == "swiglu" else L.d_ff
         st = stage if stage is not None else (lambda name: _NoStage())
         with st("ffn1"):
@@ -141,7 +275,7 @@ class EPMoELayer:
     (local slot le = global expert rank*E_l + le)."""
 
     def __init__(self, wg, pool: ExpertPool, d_ff: int, world: int, rank: int, act="relu",
-                 top_k=1, norm_topk=None, capacity_factor=1.25, group=None):
+                 top_k=1, norm_topk=None, capacity_factor=1.25, group=None, transport=None):
         from .layer import MoELayer
         d, E = wg.shape
         if E % world:
@@ -156,6 +290,12 @@ class EPMoELayer:
         self.local = MoELayer(wg, pool, d_ff, act=act, top_k=top_k, norm_topk=norm_topk,
                               capacity_factor=capacity_factor, expert_slots=[0] * E)
         self.ops = DeviceOps(self.local)
+        # "nccl": two ncclAllToAll per forward; "peer": stores / loads into the
+        # peers' HBM over NVLink (CUDA IPC) with flag barriers
+        self.transport = transport or os.environ.get("COMOE_EP_TRANSPORT", "nccl")
+        if self.transport not in ("nccl", "peer"):
+            raise ValueError(f"unknown EP transport {self.transport!r}")
+        self.peers = None
 
     @classmethod
     def synthetic(cls, wg, d_ff, E, world, rank, capacity_factor=1.25, seed=2, act="relu"):
@@ -173,9 +313,25 @@ class EPMoELayer:
     def last(self):
         return self.local.last
 
+    def peer_buffers(self, T: int) -> PeerBuffers:
+        """The peer-transport buffers for T tokens per rank (collective on
+        first use and whenever the capacity changes: every rank calls it
+        with the same T)."""
+        rows = self.E * self.capacity(T)
+        if self.peers is None or self.peers.rows != rows:
+            if self.peers is not None:
+                self.peers.close()
+            self.peers = PeerBuffers(rows, self.local.d, self.E, self.world, self.rank,
+                                     self.local.wg.device, group=self.group)
+        return self.peers
+
     def forward(self, x, out=None, timer=None):
-        y = ep_forward(x, self.ops, self.world, self.E, self.capacity(x.shape[0]),
-                       group=self.group, stage=timer)
+        C = self.capacity(x.shape[0])
+        if self.transport == "peer":
+            y = ep_forward_peers(x, self.ops, self.peer_buffers(x.shape[0]), self.E, C,
+                                 stage=timer)
+        else:
+            y = ep_forward(x, self.ops, self.world, self.E, C, group=self.group, stage=timer)
         if out is not None:
             out.copy_(y)
             return out

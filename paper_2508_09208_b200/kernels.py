@@ -209,6 +209,75 @@ def combine(y_perm, token_pos, gate_prob, out=None) -> torch.Tensor:
     return out
 
 
+# ---------------------------------------------------------------- EP over peer memory
+
+def permute_peers(x, gate: GateOutput, scan: ScanOutput, capacity: int, peer_rows,
+                  block_rows: int, src_rank: int, out: PermuteOutput):
+    """K2 with every kept row stored into its owner's receive buffer:
+    `peer_rows` is an int64 device tensor of the world's receive-buffer
+    addresses (see include/comoe_b200.h, EP over NVLink peer memory).
+    `out.x_perm` is unused; row_token / row_prob / token_pos are local."""
+    _need(x, "x", torch.bfloat16, 2)
+    _need(peer_rows, "peer_rows", torch.int64, 1)
+    T, d = x.shape
+    k = gate.group_idx.shape[1]
+    G = scan.group_base.numel()
+    _lib.call("comoe_permute_peers", _ptr(x), T, d, k, _ptr(gate.group_idx), _ptr(gate.gate_prob),
+              _ptr(gate.local_rank), _ptr(scan.tile_offset), _ptr(scan.group_base), G,
+              int(capacity), _ptr(peer_rows), peer_rows.numel(), int(block_rows), int(src_rank),
+              _ptr(out.row_token), _ptr(out.row_prob), _ptr(out.token_pos), _stream())
+    return out
+
+
+def combine_peers(peer_rows, block_rows: int, src_rank: int, token_pos, gate_prob, d: int,
+                  out=None) -> torch.Tensor:
+    """K4 reading each kept row from its owner's output buffer."""
+    _need(peer_rows, "peer_rows", torch.int64, 1)
+    _need(token_pos, "token_pos", torch.int32, 2)
+    _need(gate_prob, "gate_prob", torch.float32, 2)
+    T, k = token_pos.shape
+    if out is None:
+        out = torch.empty((T, d), dtype=torch.bfloat16, device=token_pos.device)
+    _lib.call("comoe_combine_peers", _ptr(peer_rows), peer_rows.numel(), int(block_rows),
+              int(src_rank), _ptr(token_pos), _ptr(gate_prob), T, d, k, _ptr(out), _stream())
+    return out
+
+
+def peer_scatter_counts(counts, world: int, src_rank: int, peer_counts) -> None:
+    _need(counts, "counts", torch.int32, 1)
+    _need(peer_counts, "peer_counts", torch.int64, 1)
+    _lib.call("comoe_peer_scatter_counts", _ptr(counts), counts.numel(), int(world),
+              int(src_rank), _ptr(peer_counts), _stream())
+
+
+def peer_barrier(pads, world: int, rank: int, epoch: int, err, timeout_s: float = 10.0) -> None:
+    """Stream-ordered flag barrier over peer memory; a peer that does not
+    arrive within `timeout_s` sets err[0] = 1 + peer instead of hanging."""
+    _need(pads, "pads", torch.int64, 1)
+    _need(err, "err", torch.int32, 1)
+    _lib.call("comoe_peer_barrier", _ptr(pads), int(world), int(rank), int(epoch),
+              int(timeout_s * 1e9), _ptr(err), _stream())
+
+
+def ipc_handle(t: torch.Tensor):
+    """(handle bytes, offset) naming the allocation that holds `t`."""
+    n = _lib.load().comoe_ipc_handle_size()
+    buf = ctypes.create_string_buffer(n)
+    off = ctypes.c_long(0)
+    _lib.call("comoe_ipc_get_handle", _ptr(t), buf, ctypes.byref(off))
+    return bytes(buf.raw), int(off.value)
+
+
+def ipc_open(handle: bytes, offset: int) -> int:
+    ptr = ctypes.c_void_p(0)
+    _lib.call("comoe_ipc_open", handle, int(offset), ctypes.byref(ptr))
+    return int(ptr.value)
+
+
+def ipc_close(ptr: int, offset: int) -> None:
+    _lib.call("comoe_ipc_close", int(ptr), int(offset))
+
+
 # ---------------------------------------------------------------- K3
 
 def expert_numel(d: int, d_ff: int, act: int) -> int:
