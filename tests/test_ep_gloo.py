@@ -119,3 +119,46 @@ def test_ep_forward_world2_gloo():
     for rank, err, dropped in res:
         assert err < 1e-5, (rank, err)
         assert dropped > 0  # capacity factor 1.0 forces drops: the per-group rule is exercised
+
+
+def _peer_worker(rank, world, port, q):
+    """PeerBuffers' handle exchange over gloo with the IPC calls stubbed: the
+    pointer tables must list every rank's buffers in rank order (own buffers
+    by address, peers' through ipc_open of their handle + offset)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2508_09208_b200 import kernels
+        from paper_2508_09208_b200.ep import PeerBuffers
+        opened = []
+        kernels.ipc_handle = lambda t: (f"r{rank}:{t.numel()}".encode(), 100 + rank)
+        kernels.ipc_open = lambda h, off: opened.append((h, off)) or (1 << 40) + 1000 * int(h[1:2]) + off
+        b = PeerBuffers(world * 6, 16, 4 * world, world, rank, torch.device("cpu"))
+        res = {f: getattr(b, f + "_ptrs").tolist() for f in PeerBuffers._FIELDS}
+        q.put((rank, res, {f: getattr(b, f).data_ptr() for f in PeerBuffers._FIELDS},
+               sorted(opened), len(b._opened)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_buffers_handle_exchange_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    world = 3
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, ptrs, own, opened, n_open in res:
+        assert n_open == 4 * (world - 1)
+        for f, table in ptrs.items():
+            assert len(table) == world
+            for qr in range(world):
+                if qr == rank:
+                    assert table[qr] == own[f]
+                else:  # the fake mapping of rank qr's handle at its offset
+                    assert table[qr] == (1 << 40) + 1000 * qr + 100 + qr
