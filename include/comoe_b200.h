@@ -194,6 +194,13 @@ int comoe_merge(int dtype, const void* const* member_ptrs, const int* group_offs
  * where materialising the reference's n x D fp64 calibration is infeasible.
  */
 long comoe_sim_workspace_bytes(int E, int n_probes, int buckets, long D);
+/* Cosine Gram of 9..128 bf16 experts stored as consecutive rows of one
+ * stride (a layer's pool slots): expert e at base + e * row_stride
+ * (elements). tcgen05 split-K, fp64 result in gram[E,E]; work:
+ * comoe_sim_workspace_bytes(E, 0, 0, D) bytes. */
+int comoe_sim_tc_supported(int E, long D);
+int comoe_sim_gram_strided(const void* base, long row_stride, int E, long D, double* gram,
+                           void* work, void* stream);
 int comoe_sim_contract(int dtype, const void* const* rows, int E, long D, const double* probes,
                        int n_probes, const double* proj, int buckets, double* gram,
                        double* logits, void* work, void* stream);

@@ -51,6 +51,8 @@ _SIGNATURES = {
     "comoe_sim_workspace_bytes": [_c_int, _c_int, _c_int, _c_long],
     "comoe_sim_contract": [_c_int, _p, _c_int, _c_long, _p, _c_int, _p, _c_int, _p, _p, _p,
                            _p],
+    "comoe_sim_tc_supported": [_c_int, _c_long],
+    "comoe_sim_gram_strided": [_p, _c_long, _c_int, _c_long, _p, _p, _p],
     "comoe_sim_finalize": [_p, _p, _c_int, _c_int, _c_int, _c_double, _p, _p],
     "comoe_predictor_workspace_bytes": [_c_int, _c_int],
     "comoe_predictor_mlp": [_p, _c_int, _c_int, _p, _c_int, _p, _c_int, _p, _p, _c_int, _p,

@@ -8,9 +8,10 @@
 // computed in 32x32 output tiles over D-slices, then reduced over slices in a
 // fixed order (deterministic). Always accumulated in fp64 (the reference is
 // fp64 and its surrogate softmax is sensitive to logit error).
+#include <cstdlib>
 #include <utility>
 
-#include "common.cuh"
+#include "grouped_gemm.cuh"
 #include "../../include/comoe_b200.h"
 
 namespace comoe {
@@ -226,8 +227,11 @@ __global__ void __launch_bounds__(128) sim_gram_mma_kernel(const void* const* __
   const bool diag = ti == tj;
   const int g = lane >> 2, tq = lane & 3;
   const int I0 = ti * T, J0 = tj * T;
-  const long d0 = split * slice;
-  const long d1 = d0 + slice < D ? d0 + slice : D;
+  // interleaved 32U-d chunks (split, split + splits, ...): concurrent warps
+  // read neighbouring pieces of each row (DRAM page locality)
+  const long d0 = static_cast<long>(split) * 32 * U;
+  const long dstep = static_cast<long>(splits) * 32 * U;
+  const long d1 = D;
   const int4* ra[Q];
   const int4* rb[Q];
 #pragma unroll
@@ -246,7 +250,7 @@ __global__ void __launch_bounds__(128) sim_gram_mma_kernel(const void* const* __
       for (int r = 0; r < 4; ++r) { c[m][n][r] = 0.f; acc[m][n][r] = 0.0; }
   const int4 z = make_int4(0, 0, 0, 0);
   int since = 0;
-  for (long d = d0; d < d1; d += 32 * U) {
+  for (long d = d0; d < d1; d += dstep) {
     int4 A[U][Q], B[U][Q];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -303,6 +307,145 @@ __global__ void __launch_bounds__(128) sim_gram_mma_kernel(const void* const* __
           if (i < E && j < E && i < I0 + T)
             out[static_cast<long>(i) * E + j] = acc[m][n][r] + static_cast<double>(c[m][n][r]);
       }
+}
+
+// Cosine Gram of 9..128 bf16 experts on the 5th-gen tensor cores
+// (tcgen05, 1-SM, M = N = 128: the expert tile is both operands), for
+// experts stored as consecutive rows of one stride (a layer's pool slots,
+// the rows of a matrix).
+// - Split-K over CTAs by interleaved 64-d blocks (block c, c + grid, ...).
+// - Warp 0: one TMA box per block (E rows x 64 d, 128-byte swizzled
+//   K-major; rows >= E stay zero). One-row boxes measured TMA-issue-bound
+//   at ~1 op / 50 cycles / SM.
+// - Warp 1: four MMAs per block into a fresh TMEM accumulator (4 of them),
+//   so the tensor core's fp32 sums stay as short as the mma.sync path's
+//   (accumulating 256 d in TMEM drifted 4e-7 relative on the diagonal).
+// - Warps 2-9 (two per TMEM lane quadrant, 64 columns each): add the two
+//   blocks of a group with one RN fp32 add, convert once (fp32 -> fp64
+//   runs on the XU pipe, which bounded a per-block fold) and accumulate in
+//   fp64 registers. The bf16 x bf16 products are exact.
+// Each CTA writes its fp64 [E,E] partial; sim_reduce_kernel sums them in a
+// fixed order. Every row is read once (the mma.sync tiles re-read each row
+// ~5x at E = 128).
+constexpr int kGtStages = 8;
+constexpr int kGtTile = 128 * 128;  // bytes per stage (128 rows x 64 bf16)
+constexpr int kGtSmem = 1024 + kGtStages * kGtTile + 256;
+constexpr int kGtThreads = 10 * 32;
+
+__global__ void __launch_bounds__(kGtThreads, 1)
+    sim_gram_tc_kernel(const __grid_constant__ CUtensorMap tmap, int row0, int box_rows, int E,
+                       long n_kb, double* __restrict__ partial) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* tiles = smem;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kGtStages * kGtTile);
+  uint64_t* empty_bar = full_bar + kGtStages;
+  uint64_t* tfull_bar = empty_bar + kGtStages;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = static_cast<int>((n_kb - blockIdx.x + gridDim.x - 1) / gridDim.x);
+
+  if (box_rows < 128)
+    for (int i = threadIdx.x; i < kGtStages * kGtTile / 16; i += blockDim.x)
+      reinterpret_cast<int4*>(tiles)[i] = make_int4(0, 0, 0, 0);  // rows >= E stay zero
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmap);
+    for (int s = 0; s < kGtStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], 8);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // zeroed rows -> async proxy
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer: the stage is one box
+    if (lane == 0) {
+      for (int i = 0; i < n; ++i) {
+        const int s = i % kGtStages;
+        if (i >= kGtStages) mbar_wait(&empty_bar[s], ((i / kGtStages) - 1) & 1);
+        mbar_expect_tx(&full_bar[s], static_cast<uint32_t>(box_rows) * 128u);
+        const int x = static_cast<int>((blockIdx.x + static_cast<long>(i) * gridDim.x) * 64);
+        tma_load_2d(tiles + s * kGtTile, &tmap, &full_bar[s], x, row0);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer
+    if (elect_one()) {
+      constexpr uint32_t kIdesc = umma_idesc_bf16_f32(128, 128);
+      for (int i = 0; i < n; ++i) {
+        // block i -> its own accumulator i % 4; blocks 2g, 2g+1 form fold
+        // group g, handed over through the pair's barriers (g % 2)
+        const int s = i % kGtStages, a = i & 3, g = i >> 1, pr = g & 1;
+        if ((i & 1) == 0) mbar_wait(&tempty_bar[pr], ((g >> 1) & 1) ^ 1);
+        mbar_wait(&full_bar[s], (i / kGtStages) & 1);
+        tc_fence_after();
+        const uint64_t desc = umma_desc_k_sw128(smem_u32(tiles + s * kGtTile));
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          umma_bf16(tmem_base + a * 128, desc + 2 * k, desc + 2 * k, kIdesc, k != 0 ? 1u : 0u);
+        umma_commit(&empty_bar[s]);
+        if ((i & 1) == 1 || i == n - 1) umma_commit(&tfull_bar[pr]);
+      }
+    }
+  } else {
+    // ------------------------------------------------ fp64 fold (warps 2-9)
+    const int q = warp & 3, h = (warp - 2) >> 2;  // lane quadrant, column half
+    const int row = q * 32 + lane;
+    double acc[64];
+#pragma unroll
+    for (int c = 0; c < 64; ++c) acc[c] = 0.0;
+    const int n_groups = (n + 1) >> 1;
+    for (int g = 0; g < n_groups; ++g) {
+      const int pr = g & 1;
+      const bool two = 2 * g + 1 < n;
+      mbar_wait(&tfull_bar[pr], (g >> 1) & 1);
+      tc_fence_after();
+      const uint32_t t = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + 2 * pr * 128 + h * 64;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        uint32_t v[32], w[32];
+        tmem_ld32(t + half * 32, v);
+        tmem_ld32(t + 128 + half * 32, w);  // block 2g+1 (unused when absent)
+        tmem_ld_wait();
+        if (half == 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty_bar[pr]);
+        }
+        // one RN fp32 add of the two 64-d block sums, then one conversion:
+        // half the XU-pipe F2F work of folding every block
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const float x = __uint_as_float(v[c]) + (two ? __uint_as_float(w[c]) : 0.f);
+          acc[half * 32 + c] += static_cast<double>(x);
+        }
+      }
+    }
+    if (row < E) {
+      double* out = partial + static_cast<long>(blockIdx.x) * E * E + static_cast<long>(row) * E;
+#pragma unroll
+      for (int c = 0; c < 64; ++c)
+        if (h * 64 + c < E) out[h * 64 + c] = acc[c];
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem_base);
+  }
 }
 
 // Surrogate logits for E <= 8 experts and <= 8 buckets (the reference's
@@ -572,6 +715,21 @@ static bool sim_mma(int dtype, int n_probes, long D) {
   return dtype == COMOE_DTYPE_BF16 && n_probes == 0 && D % 8 == 0;
 }
 
+// tcgen05 Gram for 9..128 bf16 experts (COMOE_SIM_TC=0: the mma.sync tiles)
+static bool sim_tc(int dtype, int E, long D) {
+  static const bool on = [] {
+    const char* e = std::getenv("COMOE_SIM_TC");
+    return !(e && e[0] == '0');
+  }();
+  return on && dtype == COMOE_DTYPE_BF16 && D % 8 == 0 && E > 8 && E <= 128;
+}
+
+static int gram_tc_ctas(long D) {
+  const long n_kb = (D + 63) / 64;
+  const long c = n_kb < num_sms() ? n_kb : num_sms();
+  return static_cast<int>(c > 0 ? c : 1);
+}
+
 struct GramPlan {
   int tiles_1d, splits;
   long slice;
@@ -727,6 +885,8 @@ long comoe_sim_workspace_bytes(int E, int n_probes, int buckets, long D) {
     const GramPlan g = gram_plan(E, D);
     const long wm = static_cast<long>(g.splits) * E * E * sizeof(double);
     w = w > wm ? w : wm;
+    const long wt = static_cast<long>(gram_tc_ctas(D)) * E * E * sizeof(double);
+    w = w > wt ? w : wt;
   }
   if (sim_small(E, 0)) {
     const long ws = static_cast<long>(sim_small_blocks(D)) * (E * (E + 1) / 2) * sizeof(double);
@@ -735,6 +895,40 @@ long comoe_sim_workspace_bytes(int E, int n_probes, int buckets, long D) {
   if (n_probes > 0) w += logit_plan(D).second * static_cast<long>(E) * n_probes * buckets * sizeof(double);
   return w;
 }
+
+int comoe_sim_gram_strided(const void* base, long row_stride, int E, long D, double* gram,
+                           void* work, void* stream) {
+  using namespace comoe;
+  COMOE_REQUIRE(base && gram && work, kBadArg, "sim_gram_strided: null pointer");
+  COMOE_REQUIRE(sim_tc(COMOE_DTYPE_BF16, E, D), kUnsupportedShape,
+                "sim_gram_strided: needs bf16, 8 < E <= 128, D %% 8 == 0 (E=%d D=%ld)", E, D);
+  COMOE_REQUIRE(row_stride >= D && row_stride % 8 == 0, kBadArg,
+                "sim_gram_strided: row stride %ld", row_stride);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int box_rows = (E + 7) / 8 * 8;
+  CUtensorMap tmap;
+  int rc = make_tmap_bf16_2d_box(&tmap, base, static_cast<uint64_t>(E), static_cast<uint64_t>(D),
+                                 static_cast<uint64_t>(row_stride), 64,
+                                 static_cast<uint32_t>(box_rows), 128);
+  if (rc) return rc;
+  const int ctas = gram_tc_ctas(D);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(sim_gram_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGtSmem);
+    attr = true;
+  }
+  double* partial = static_cast<double*>(work);
+  sim_gram_tc_kernel<<<ctas, kGtThreads, kGtSmem, s>>>(tmap, 0, box_rows, E, (D + 63) / 64,
+                                                        partial);
+  rc = check_launch("sim_gram_tc_kernel");
+  if (rc) return rc;
+  const long nn = static_cast<long>(E) * E;
+  const int blocks = static_cast<int>((nn + 7) / 8 < 4096 ? (nn + 7) / 8 : 4096);
+  sim_reduce_kernel<<<blocks, 256, 0, s>>>(partial, ctas, E, E, 0, gram, nullptr);
+  return check_launch("sim_reduce_kernel");
+}
+
+int comoe_sim_tc_supported(int E, long D) { return comoe::sim_tc(COMOE_DTYPE_BF16, E, D) ? 1 : 0; }
 
 int comoe_sim_contract(int dtype, const void* const* rows, int E, long D, const double* probes,
                        int n_probes, const double* proj, int buckets, double* gram,

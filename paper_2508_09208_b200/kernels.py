@@ -389,6 +389,20 @@ def merge_groups(groups_members, weights, divisors, outs, dtype) -> None:
 
 # ---------------------------------------------------------------- K6 similarity
 
+def _shared_stride(rows):
+    """(base address, row stride in elements) when the bf16 rows are
+    consecutive rows of one 16-byte-multiple stride no shorter than a row
+    (a layer's pool slots, the rows of a matrix); else None."""
+    ptrs = [r.data_ptr() for r in rows]
+    D = rows[0].numel()
+    stride = ptrs[1] - ptrs[0] if len(ptrs) > 1 else 2 * D
+    if stride % 16 or stride < 2 * D or ptrs[0] % 16:
+        return None
+    if any(p != ptrs[0] + i * stride for i, p in enumerate(ptrs)):
+        return None
+    return ptrs[0], stride // 2
+
+
 def similarity(rows, probes, proj, alpha):
     """rows: list of E flat expert tensors (bf16 or float64, same numel);
     probes [n, D], proj [B, D] float64 on the device. Returns (S, gram,
@@ -412,15 +426,22 @@ def similarity(rows, probes, proj, alpha):
     else:
         probes = proj = None
     dev = rows[0].device
-    t_rows = torch.tensor([r.data_ptr() for r in rows], dtype=torch.int64).to(dev)
     ws = _lib.load().comoe_sim_workspace_bytes(E, n, B, D)
     work = torch.empty(max(ws, 8), dtype=torch.uint8, device=dev)
     gram = torch.empty((E, E), dtype=torch.float64, device=dev)
     logits = torch.empty((E, n, B), dtype=torch.float64, device=dev) if n else None
     sim = torch.empty((E, E), dtype=torch.float64, device=dev)
-    code = DTYPE_BF16 if dt == torch.bfloat16 else DTYPE_F64
-    _lib.call("comoe_sim_contract", code, _ptr(t_rows), E, D, _ptr(probes), n, _ptr(proj), B,
-              _ptr(gram), _ptr(logits), _ptr(work), _stream())
+    strided = _shared_stride(rows) if (dt == torch.bfloat16 and n == 0 and
+                                       _lib.load().comoe_sim_tc_supported(E, D)) else None
+    if strided is not None:  # tcgen05 Gram over a tensor map of the consecutive rows
+        base, stride = strided
+        _lib.call("comoe_sim_gram_strided", ctypes.c_void_p(base), stride, E, D, _ptr(gram),
+                  _ptr(work), _stream())
+    else:
+        t_rows = torch.tensor([r.data_ptr() for r in rows], dtype=torch.int64).to(dev)
+        code = DTYPE_BF16 if dt == torch.bfloat16 else DTYPE_F64
+        _lib.call("comoe_sim_contract", code, _ptr(t_rows), E, D, _ptr(probes), n, _ptr(proj), B,
+                  _ptr(gram), _ptr(logits), _ptr(work), _stream())
     _lib.call("comoe_sim_finalize", _ptr(gram), _ptr(logits), E, n, B, float(alpha), _ptr(sim),
               _stream())
     return sim, gram, logits
