@@ -448,6 +448,111 @@ __global__ void __launch_bounds__(kGtThreads, 1)
   }
 }
 
+// Cosine Gram of <= 8 bf16 experts (C1: Switch-Base-8, C5: Mixtral 8
+// experts): a streaming kernel. Each CTA takes 2048-d chunks c, c + grid,
+// ... (interleaved: concurrent CTAs read neighbouring pieces of every row);
+// one thread moves a chunk of every row with one bulk copy per row (4 KB,
+// cp.async.bulk, completion on the stage's mbarrier; rows padded by 16 B
+// so the fragment loads are conflict-free). Consumer warp w takes 256 d of
+// the chunk: per 16 d one 8-byte shared load per lane and one mma.sync
+// m16n8k16 whose A (rows 0-7; rows 8-15 zero) and B fragments are the same
+// registers (k permuted inside the 16 d, identically for both), fp32
+// accumulation folded into fp64 every 64 d (exact bf16 products, <= 64-term
+// fp32 sums). Fixed-order CTA reduction to one fp64 [E,E] partial per CTA.
+// (The 8x8 mma.sync tiles over global memory stalled at ~1 TB/s on 16-byte
+// outstanding requests; an FFMA version was issue-bound at 3.2 TB/s.)
+constexpr int kG8Chunk = 2048, kG8Stages = 4, kG8Threads = 288;
+constexpr int kG8Pitch = kG8Chunk * 2 + 16;  // bytes per staged row
+constexpr int kG8Smem = 1024 + kG8Stages * 8 * kG8Pitch + 8 * 64 * 8 + 128;
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kG8Threads, 1)
+    sim_gram8_kernel(const void* const* __restrict__ rows, int E, long D,
+                     double* __restrict__ partial) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* tiles = smem;  // [stage][8 rows][kG8Pitch]
+  double* red = reinterpret_cast<double*>(smem + kG8Stages * 8 * kG8Pitch);  // [8 warps][64]
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(red + 8 * 64);
+  uint64_t* empty_bar = full_bar + kG8Stages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long n_chunks = (D + kG8Chunk - 1) / kG8Chunk;
+  const int n = static_cast<int>((n_chunks - blockIdx.x + gridDim.x - 1) / gridDim.x);
+  if (E < 8)
+    for (int i = threadIdx.x; i < kG8Stages * 8 * kG8Pitch / 16; i += blockDim.x)
+      reinterpret_cast<int4*>(tiles)[i] = make_int4(0, 0, 0, 0);  // rows >= E read as zero
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kG8Stages; ++st) {
+      mbar_init(&full_bar[st], 1);
+      mbar_init(&empty_bar[st], 8);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int i = 0; i < n; ++i) {
+        const int st = i % kG8Stages;
+        if (i >= kG8Stages) mbar_wait(&empty_bar[st], ((i / kG8Stages) - 1) & 1);
+        const long d0 = (blockIdx.x + static_cast<long>(i) * gridDim.x) * kG8Chunk;
+        const long len = D - d0 < kG8Chunk ? D - d0 : kG8Chunk;
+        const uint32_t bytes = static_cast<uint32_t>(len * 2);
+        mbar_expect_tx(&full_bar[st], bytes * static_cast<uint32_t>(E));
+        for (int e = 0; e < E; ++e)
+          bulk_load(tiles + (st * 8 + e) * kG8Pitch,
+                    static_cast<const __nv_bfloat16*>(rows[e]) + d0, bytes, &full_bar[st]);
+      }
+    }
+    return;
+  }
+  const int w = warp - 1;                  // 256 d of every chunk
+  const int g = lane >> 2, tq = lane & 3;  // fragment row / k quad
+  float c[4] = {0.f, 0.f, 0.f, 0.f};
+  double acc[2] = {0.0, 0.0};
+  for (int i = 0; i < n; ++i) {
+    const int st = i % kG8Stages;
+    const long d0 = (blockIdx.x + static_cast<long>(i) * gridDim.x) * kG8Chunk;
+    const int len = static_cast<int>(D - d0 < kG8Chunk ? D - d0 : kG8Chunk);
+    mbar_wait(&full_bar[st], (i / kG8Stages) & 1);
+    const uint8_t* row = tiles + (st * 8 + g) * kG8Pitch;
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      const int d = w * 256 + kk * 16 + 4 * tq;  // this lane's 4 d of the 16-d step
+      uint2 v = make_uint2(0u, 0u);
+      if (d < len) v = *reinterpret_cast<const uint2*>(row + 2 * d);
+      mma_bf16_16816(c, v.x, 0u, v.y, 0u, v.x, v.y);
+      if ((kk & 3) == 3) {  // fold every 64 d
+        acc[0] += static_cast<double>(c[0]);
+        acc[1] += static_cast<double>(c[1]);
+        c[0] = c[1] = c[2] = c[3] = 0.f;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[st]);
+  }
+  // lane holds C[g][2tq], C[g][2tq+1]; the 8 warps are summed in a fixed order
+  red[w * 64 + g * 8 + 2 * tq] = acc[0];
+  red[w * 64 + g * 8 + 2 * tq + 1] = acc[1];
+  asm volatile("bar.sync 1, 256;" ::: "memory");  // consumer warps only
+  const int t = threadIdx.x - 32;
+  if (t < 64) {
+    double v = 0.0;
+    for (int ww = 0; ww < 8; ++ww) v += red[ww * 64 + t];
+    const int a = t >> 3, b = t & 7;
+    if (a < E && b < E) partial[static_cast<long>(blockIdx.x) * E * E + a * E + b] = v;
+  }
+}
+
 // Surrogate logits for E <= 8 experts and <= 8 buckets (the reference's
 // defaults): logits[e][n][b] = sum_d P[e,d] probes[n,d] proj[b,d]. A block
 // owns a contiguous D-slice and streams it in 256-d chunks through a
@@ -724,6 +829,21 @@ static bool sim_tc(int dtype, int E, long D) {
   return on && dtype == COMOE_DTYPE_BF16 && D % 8 == 0 && E > 8 && E <= 128;
 }
 
+// streaming Gram for <= 8 bf16 experts (COMOE_SIM_G8=0: the mma.sync tiles)
+static bool sim_g8(int dtype, int E, long D) {
+  static const bool on = [] {
+    const char* e = std::getenv("COMOE_SIM_G8");
+    return !(e && e[0] == '0');
+  }();
+  return on && dtype == COMOE_DTYPE_BF16 && D % 8 == 0 && E >= 1 && E <= 8;
+}
+
+static int gram8_ctas(long D) {
+  const long n = (D + kG8Chunk - 1) / kG8Chunk;
+  const long c = n < num_sms() ? n : num_sms();
+  return static_cast<int>(c > 0 ? c : 1);
+}
+
 static int gram_tc_ctas(long D) {
   const long n_kb = (D + 63) / 64;
   const long c = n_kb < num_sms() ? n_kb : num_sms();
@@ -838,6 +958,21 @@ static int tiled_contract(int dtype, const void* const* rows, int E, long D, con
 // fp64 tiles otherwise) into gram[E,E]
 static int gram_contract(int dtype, const void* const* rows, int E, long D, double* gram,
                          double* partial, cudaStream_t s) {
+  if (sim_g8(dtype, E, D)) {
+    const int ctas = gram8_ctas(D);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(sim_gram8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kG8Smem);
+      attr = true;
+    }
+    sim_gram8_kernel<<<ctas, kG8Threads, kG8Smem, s>>>(rows, E, D, partial);
+    int rc = check_launch("sim_gram8_kernel");
+    if (rc) return rc;
+    const long n = static_cast<long>(E) * E;
+    const int blocks = static_cast<int>((n + 7) / 8 < 4096 ? (n + 7) / 8 : 4096);
+    sim_reduce_kernel<<<blocks, 256, 0, s>>>(partial, ctas, E, E, 0, gram, nullptr);
+    return check_launch("sim_reduce_kernel");
+  }
   if (sim_mma(dtype, 0, D)) {
     const GramPlan gp = gram_plan(E, D);
     const long units = static_cast<long>(gp.tiles_1d) * (gp.tiles_1d + 1) / 2 * gp.splits;
@@ -887,6 +1022,8 @@ long comoe_sim_workspace_bytes(int E, int n_probes, int buckets, long D) {
     w = w > wm ? w : wm;
     const long wt = static_cast<long>(gram_tc_ctas(D)) * E * E * sizeof(double);
     w = w > wt ? w : wt;
+    const long w8 = static_cast<long>(gram8_ctas(D)) * E * E * sizeof(double);
+    w = w > w8 ? w : w8;
   }
   if (sim_small(E, 0)) {
     const long ws = static_cast<long>(sim_small_blocks(D)) * (E * (E + 1) / 2) * sizeof(double);
