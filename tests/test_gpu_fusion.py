@@ -238,3 +238,25 @@ def test_predictor_any_demand_mode():
     p = probs.cpu().numpy()
     ref = -np.expm1(np.log1p(-p).sum(0))
     np.testing.assert_allclose(demand.cpu().numpy(), ref, rtol=1e-10, atol=1e-14)
+
+
+@pytest.mark.parametrize("E,D", [(9, 5 * 64 + 8), (128, 2048 + 8), (2, 2040), (1, 16), (8, 3 * 2048 + 24),
+                                 (40, 64)])
+def test_similarity_cosine_edge_shapes(E, D):
+    """Gram paths at their edges: the tcgen05 path's smallest / largest E and
+    a ragged last 64-d block, the streaming <= 8 path with a D shorter than
+    one 2048-d chunk and with a ragged last chunk, a single expert, and the
+    non-consecutive-row fallback (rows gathered out of order)."""
+    from paper_2508_09208_b200 import kernels
+    g = torch.Generator(device="cuda").manual_seed(100 + E)
+    V = (torch.randn(E, D, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+    Vh = V.double().cpu().numpy()
+    G = Vh @ Vh.T
+    for order in (list(range(E)), list(reversed(range(E)))):
+        sim, gram, _ = kernels.similarity([V[e] for e in order], None, None, 1.0)
+        Go = G[np.ix_(order, order)]
+        # fp32 sums of <= 64 exact products per block: ~1 fp32 ulp of a block
+        # partial per block, which at short D is ~1e-8 of the Gram scale
+        np.testing.assert_allclose(gram.cpu().numpy(), Go, rtol=1e-6, atol=3e-8 * np.abs(G).max())
+        np.testing.assert_allclose(sim.cpu().numpy(), M.cosine_matrix(Vh[order]), rtol=1e-7,
+                                   atol=1e-7)
