@@ -56,3 +56,19 @@ def test_product_never_imports_the_oracle():
     for p in (ROOT / "paper_2508_09208_b200").rglob("*.py"):
         src = p.read_text()
         assert not re.search(r"^\s*(from|import)\s+oracle", src, re.M), p
+
+
+def test_similarity_row_layout_detection():
+    """kernels._shared_stride picks the tcgen05 Gram only for consecutive
+    rows of one 16-byte-multiple stride (pool slots, rows of a matrix)."""
+    import torch
+    from paper_2508_09208_b200 import kernels
+    P = torch.zeros(6, 1024, dtype=torch.bfloat16)
+    base, stride = kernels._shared_stride([P[i] for i in range(6)])
+    assert base == P.data_ptr() and stride == 1024
+    pool = torch.zeros(8, 1536, dtype=torch.bfloat16)  # slot stride > row length
+    assert kernels._shared_stride([pool[i, :1024] for i in range(2, 6)])[1] == 1536
+    assert kernels._shared_stride([P[i] for i in (0, 2, 1)]) is None   # out of order
+    assert kernels._shared_stride([P[i] for i in (0, 2, 4)])[1] == 2048  # every other row
+    Q = torch.zeros(4, 1028, dtype=torch.bfloat16)  # 2056-byte stride: not 16-byte aligned
+    assert kernels._shared_stride([Q[i] for i in range(4)]) is None
