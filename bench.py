@@ -6,8 +6,11 @@ Workload = BASELINE.json configs[1] (C2): Switch-Base-128-shaped MoE layer
 (d_model 768, d_ff 3072, 128 experts, top-1, capacity factor 1.25), 65,536
 synthetic tokens per GPU, all experts HBM-resident, random-init weights.
 A step = one layer forward (gate -> scan -> permute -> grouped FFN with the
-fused combine) over one batch. N>1 (torchrun) = expert parallelism with NCCL
-all-to-all dispatch/combine, 65,536 tokens per GPU (weak scaling).
+fused combine) over one batch; on one GPU each step is one CUDA-graph replay
+of the forward (MoELayer.capture; `--eager` launches the kernels one by one,
+and the per-stage kernel times come from an eager pass of the same K steps).
+N>1 (torchrun) = expert parallelism with NCCL all-to-all dispatch/combine,
+65,536 tokens per GPU (weak scaling).
 
 `--impl reference` times the reference CPU path of this layer on the host
 cores (the oracle port, oracle/switch_layer.layer_forward_fast: the
@@ -43,6 +46,8 @@ def _args():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--eager", action="store_true",
+                    help="time eager launches instead of CUDA-graph replays of the forward")
     ap.add_argument("--force-ep", action="store_true",
                     help="dev: run the expert-parallel layer (NCCL) even at one GPU")
     return ap.parse_args()
@@ -239,16 +244,39 @@ def run_ours(args):
     for _ in range(args.warmup):
         layer.forward(x, out=y)
     barrier()
+    # single-GPU serving runs the forward as one CUDA-graph replay per batch
+    # (MoELayer.capture); the EP path launches eagerly (NCCL all-to-alls)
+    cap = None
+    if not (args.eager or world > 1 or args.force_ep):
+        cap = layer.capture(x, y)
+        for _ in range(args.warmup):
+            cap.replay()
+        barrier()
 
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
         start.record(stream)
         for _ in range(args.steps):
-            layer.forward(x, out=y, timer=_Stage)
+            if cap is not None:
+                cap.replay()
+            else:
+                layer.forward(x, out=y, timer=_Stage)
         end.record(stream)
         barrier()
     ms = start.elapsed_time(end) / args.steps
+    eager_ms = None
+    if cap is not None:
+        # per-kernel times: the same K forwards launched eagerly with CUDA events
+        # around every stage on the launching stream (graph replays carry none)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            layer.forward(x, out=y, timer=_Stage)
+        e1.record(stream)
+        barrier()
+        eager_ms = e0.elapsed_time(e1) / args.steps
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -284,7 +312,7 @@ def run_ours(args):
         from paper_2508_09208_b200.stream import HostPipeline
         xh = x.cpu().pin_memory()
         yhs = [torch.empty_like(xh).pin_memory() for _ in range(2)]
-        pipe = HostPipeline(layer, T_PER_GPU, D, device=dev)
+        pipe = HostPipeline(layer, T_PER_GPU, D, device=dev, graphs=cap is not None)
         pipe.run([xh] * 3, [yhs[i % 2] for i in range(3)])  # warm-up
         pipe.synchronize()
         barrier()
@@ -305,7 +333,8 @@ def run_ours(args):
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
                "ms_per_step": ms_e2e, "matches_device_forward": ok,
                "path": "paper_2508_09208_b200.stream.HostPipeline: pinned host x -> H2D -> "
-                       "MoELayer.forward -> D2H y, 3 streams, depth 2"}
+                       + ("captured MoELayer forward (graph replay)" if cap is not None
+                          else "MoELayer.forward") + " -> D2H y, 3 streams, depth 2"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -325,6 +354,8 @@ def run_ours(args):
             "config": _config(world), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk.summary(),
             "stages_ms": stages, "kept_rows": kept,
+            "launch": "cuda-graph replay per step (MoELayer.capture)" if cap is not None else "eager",
+            "eager_ms_per_step": eager_ms,
         }
         _emit(line)
     if dist.is_initialized():

@@ -215,3 +215,39 @@ class MoELayer:
     def kernels_per_forward(self) -> int:
         """Device kernels one forward launches (gate, scan, permute, 2x GEMM [, combine])."""
         return 5 + (0 if self.top_k == 1 else 1)
+
+    def capture(self, x: torch.Tensor, out: torch.Tensor = None) -> "CapturedForward":
+        """Record one forward over the static buffers `x` (and `out`) as a
+        CUDA graph: `replay()` re-runs gate -> scan -> permute -> GEMMs on
+        whatever `x` holds (routing and capacity are computed on the
+        device, so every replay is a complete forward of the current
+        contents) without per-kernel launch overhead."""
+        return CapturedForward(self, x, out)
+
+
+class CapturedForward:
+    """A MoELayer forward recorded as a CUDA graph on static device buffers.
+
+    Write the batch into `.x` (e.g. the destination of an H2D copy), call
+    `replay()` on the stream that should run it, read `.y`. The layer's
+    workspace for this token count is shared with its eager forward (do not
+    run both concurrently). Measured at C2: 0.647 ms eager vs 0.627 ms per
+    replay (the five launches' gaps and host overhead)."""
+
+    def __init__(self, layer: MoELayer, x: torch.Tensor, out: torch.Tensor = None):
+        self.layer = layer
+        self.x = x
+        self.y = out if out is not None else torch.empty_like(x)
+        dev = x.device
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):  # workspace and tensor maps outside the capture
+            layer.forward(self.x, out=self.y)
+        torch.cuda.current_stream(dev).wait_stream(side)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            layer.forward(self.x, out=self.y)
+
+    def replay(self) -> torch.Tensor:
+        self.graph.replay()
+        return self.y

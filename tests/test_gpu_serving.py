@@ -100,3 +100,27 @@ def test_ep_expert_ffn_expert_major_groups_world4():
             ref = torch.relu(xs @ wi.t()).to(torch.bfloat16).float() @ wo.t()
             got = y[blk * C: blk * C + n].float()
             assert (got - ref).norm() / ref.norm() < 5e-3, (src, le)
+
+
+def test_captured_forward_replays_match_eager():
+    """MoELayer.capture: every replay is a complete forward of the current
+    contents of the static input (different batches route differently), bit
+    for bit the eager forward; the graphed host pipeline matches too."""
+    from paper_2508_09208_b200.stream import HostPipeline
+    layer, x, wg, w = _layer(4096, 256, 512, 16)
+    xs = [(x * (1 + 0.5 * i) + i).cuda() for i in range(3)]
+    xbuf = torch.empty_like(xs[0])
+    cap = layer.capture(xbuf)
+    for xi in xs:
+        xbuf.copy_(xi)
+        y = cap.replay().clone()
+        ref = layer.forward(xi)
+        torch.cuda.synchronize()
+        assert torch.equal(y, ref)
+    hx = [v.cpu().pin_memory() for v in xs]
+    hy = [torch.empty_like(v) .pin_memory() for v in hx]
+    pipe = HostPipeline(layer, 4096, 256, graphs=True)
+    pipe.run(hx, hy)
+    pipe.synchronize()
+    for xh, yh in zip(hx, hy):
+        assert torch.equal(yh, layer.forward(xh.cuda()).cpu())
