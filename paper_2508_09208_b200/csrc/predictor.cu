@@ -20,7 +20,7 @@
 namespace comoe {
 
 constexpr int kPredMaxHidden = 256;
-constexpr int kPredWarps = 8;
+constexpr int kPredWarps = 16;
 constexpr int kPredChunk = 256;  // tokens per demand partial
 constexpr int kPredEPL = 8;      // experts per lane in registers (E <= 256)
 constexpr int kPredTok = 4;      // tokens per warp pass
@@ -67,7 +67,8 @@ __global__ void __launch_bounds__(kPredWarps * 32, 2) predictor_kernel(
     for (int t0 = c * kPredChunk + warp * kPredTok; t0 < t_end; t0 += kPredWarps * kPredTok) {
       // hidden = relu(W1 x + b1): the reference's dense x.w sum, with the
       // K-hot block contributing its selected columns (x[s] = 1, duplicates once)
-      for (int h = lane; h < hidden; h += 32) {
+      for (int h0 = 0; h0 < hidden; h0 += 32) {  // warp-uniform (the shuffles below)
+        const int h = h0 + lane < hidden ? h0 + lane : hidden - 1;  // lanes past hidden: discarded
         double z[kPredTok];
 #pragma unroll
         for (int q = 0; q < kPredTok; ++q) {
@@ -81,24 +82,30 @@ __global__ void __launch_bounds__(kPredWarps * 32, 2) predictor_kernel(
             if (!dup && s >= 0 && s < E) z[q] += w1t[static_cast<long>(s) * hidden + h];
           }
         }
-        for (int j = 0; j < emb_dim; ++j) {
-          const double w = w1t[static_cast<long>(E + j) * hidden + h];
+        // dense inputs [emb | ctx] of the kPredTok tokens: 32 at a time, one
+        // coalesced load per lane, then broadcast by shuffle (each lane read
+        // every element through L1 before: a dependent load per FMA)
+        const int dense = emb_dim + ctx_dim;
+        for (int j0 = 0; j0 < dense; j0 += 32) {
+          double xv[kPredTok];
 #pragma unroll
           for (int q = 0; q < kPredTok; ++q) {
             const int t = min(t0 + q, t_end - 1);
-            z[q] = fma(w, __ldg(emb + static_cast<long>(t) * emb_dim + j), z[q]);
+            const int j = j0 + lane;
+            xv[q] = j < emb_dim ? __ldg(emb + static_cast<long>(t) * emb_dim + j)
+                    : j < dense ? __ldg(ctx + static_cast<long>(t) * ctx_dim + (j - emb_dim))
+                                : 0.0;
+          }
+          const int jn = dense - j0 < 32 ? dense - j0 : 32;
+          for (int jj = 0; jj < jn; ++jj) {
+            const double w = w1t[static_cast<long>(E + j0 + jj) * hidden + h];
+#pragma unroll
+            for (int q = 0; q < kPredTok; ++q) z[q] = fma(w, __shfl_sync(0xffffffffu, xv[q], jj), z[q]);
           }
         }
-        for (int j = 0; j < ctx_dim; ++j) {
-          const double w = w1t[static_cast<long>(E + emb_dim + j) * hidden + h];
+        if (h0 + lane < hidden)
 #pragma unroll
-          for (int q = 0; q < kPredTok; ++q) {
-            const int t = min(t0 + q, t_end - 1);
-            z[q] = fma(w, __ldg(ctx + static_cast<long>(t) * ctx_dim + j), z[q]);
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < kPredTok; ++q) hw[q * hidden + h] = z[q] > 0.0 ? z[q] : 0.0;
+          for (int q = 0; q < kPredTok; ++q) hw[q * hidden + h] = z[q] > 0.0 ? z[q] : 0.0;
       }
       __syncwarp();
       // logits = W2 h + b2 ; softmax over E. Lane owns experts lane + 32u.

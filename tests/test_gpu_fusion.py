@@ -195,13 +195,15 @@ def test_merge_many_groups_unstaged_path():
         torch.testing.assert_close(outs[i].float(), ref, rtol=1e-2, atol=1e-4)
 
 
-@pytest.mark.parametrize("E,K", [(20, 1), (64, 2), (200, 2)])
-def test_predictor_expert_counts(E, K):
-    """Every experts-per-lane instantiation, duplicate K-hot slots and a
-    ragged last token chunk."""
+@pytest.mark.parametrize("E,K,H,emb", [(20, 1, 32, 16), (64, 2, 32, 16), (200, 2, 32, 16),
+                                        (64, 2, 40, 48)])
+def test_predictor_expert_counts(E, K, H, emb):
+    """Every experts-per-lane instantiation, duplicate K-hot slots, a ragged
+    last token chunk, a hidden width that is not a multiple of 32 and more
+    than 32 dense inputs."""
     from paper_2508_09208_b200 import kernels
-    rng = np.random.default_rng(E)
-    emb, ctx, H, B = 16, 8, 32, 777
+    rng = np.random.default_rng(E + H)
+    ctx, B = 8, 777
     w1 = rng.normal(scale=0.1, size=(H, E + emb + ctx)); b1 = rng.normal(size=H) * 0.1
     w2 = rng.normal(scale=0.1, size=(E, H)); b2 = rng.normal(size=E) * 0.1
     slots = rng.integers(0, E, size=(B, K)).astype(np.int32)
