@@ -102,6 +102,28 @@ def test_ep_expert_ffn_expert_major_groups_world4():
             assert (got - ref).norm() / ref.norm() < 5e-3, (src, le)
 
 
+def test_captured_forward_top2_swiglu():
+    """Capture of the top-2 SwiGLU layer (separate combine kernel, y_perm
+    workspace): replays equal the eager forward."""
+    from paper_2508_09208_b200 import ExpertPool, MoELayer, kernels
+    g = torch.Generator().manual_seed(9)
+    T, d, d_ff, E = 3000, 256, 512, 8
+    wg = (torch.randn(d, E, generator=g) / math.sqrt(d)).cuda()
+    numel = kernels.expert_numel(d, d_ff, kernels.ACT_SWIGLU)
+    pool = ExpertPool(E, numel)
+    pool.data[:, :numel].copy_((torch.randn(E, numel, generator=g) * 0.02).to(torch.bfloat16).cuda())
+    layer = MoELayer(wg, pool, d_ff, act="swiglu", top_k=2, capacity_factor=1.0)
+    xbuf = torch.empty(T, d, dtype=torch.bfloat16, device="cuda")
+    cap = layer.capture(xbuf)
+    for i in range(2):
+        xi = torch.randn(T, d, generator=g).to(torch.bfloat16).cuda()
+        xbuf.copy_(xi)
+        y = cap.replay().clone()
+        ref = layer.forward(xi)
+        torch.cuda.synchronize()
+        assert torch.equal(y, ref)
+
+
 def test_captured_forward_replays_match_eager():
     """MoELayer.capture: every replay is a complete forward of the current
     contents of the static input (different batches route differently), bit
