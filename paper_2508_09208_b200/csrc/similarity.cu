@@ -672,6 +672,131 @@ __global__ void __launch_bounds__(512) sim_logits_small_kernel(
   }
 }
 
+// Surrogate logits on the fp64 tensor cores (bf16 parameters, <= 8
+// experts, probes and buckets): for each probe n the logits are an 8x8
+// GEMM over d, logits_n[e][b] = sum_d P[e,d] * (probe[n,d] * proj[b,d]),
+// one mma.sync.m8n8k4.f64 per probe per 4 d. A = P (lane: expert
+// lane/4, d lane%4); B_n = probe_n (.) proj formed in the fragment (lane:
+// bucket lane/4, d lane%4: one fp64 multiply per probe). One thread moves
+// each 256-d chunk of the P, probe and projection rows with bulk copies
+// (3 stages, rows padded so fragment loads do not conflict); 8 consumer
+// warps take 32 d each. fp64 throughout (the tensor-core fp64 FMA is
+// IEEE), deterministic per block (warps summed in order). The vector path
+// (2 warps per probe, 32 accumulators per lane) needed 2.5 shared-memory
+// bytes per FMA and ran at ~27% of the fp64 rate (C1: ~440 us).
+constexpr int kLdChunk = 256, kLdStages = 3, kLdThreads = 288;
+constexpr int kLdPPitch = kLdChunk * 2 + 16, kLdFPitch = kLdChunk * 8 + 32;
+constexpr int kLdStage = 8 * kLdPPitch + 16 * kLdFPitch;  // P | probes | projection
+constexpr int kLdSmem = 1024 + kLdStages * kLdStage + 8 * 8 * 64 * 8 + 128;
+
+__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void bulk_load_ld(void* dst, const void* src, uint32_t bytes,
+                                             uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kLdThreads, 1)
+    sim_logits_dmma_kernel(const void* const* __restrict__ rows, int E, long D,
+                           const double* __restrict__ probes, int n_probes,
+                           const double* __restrict__ proj, int B, long slice,
+                           double* __restrict__ partial) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  double* red = reinterpret_cast<double*>(smem + kLdStages * kLdStage);  // [8 warps][8 n][64]
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(red + 8 * 8 * 64);
+  uint64_t* empty_bar = full_bar + kLdStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long d0 = blockIdx.x * slice;
+  const long d1 = d0 + slice < D ? d0 + slice : D;
+  const int n = d1 > d0 ? static_cast<int>((d1 - d0 + kLdChunk - 1) / kLdChunk) : 0;
+  for (int i = threadIdx.x; i < kLdStages * kLdStage / 16; i += blockDim.x)
+    reinterpret_cast<int4*>(smem)[i] = make_int4(0, 0, 0, 0);  // absent rows read as zero
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kLdStages; ++st) {
+      mbar_init(&full_bar[st], 1);
+      mbar_init(&empty_bar[st], 8);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int i = 0; i < n; ++i) {
+        const int st = i % kLdStages;
+        if (i >= kLdStages) mbar_wait(&empty_bar[st], ((i / kLdStages) - 1) & 1);
+        const long c = d0 + static_cast<long>(i) * kLdChunk;
+        const long len = d1 - c < kLdChunk ? d1 - c : kLdChunk;
+        uint8_t* sb = smem + st * kLdStage;
+        mbar_expect_tx(&full_bar[st], static_cast<uint32_t>(len * (2 * E + 8 * (n_probes + B))));
+        for (int e = 0; e < E; ++e)
+          bulk_load_ld(sb + e * kLdPPitch, static_cast<const __nv_bfloat16*>(rows[e]) + c,
+                       static_cast<uint32_t>(len * 2), &full_bar[st]);
+        for (int q = 0; q < n_probes; ++q)
+          bulk_load_ld(sb + 8 * kLdPPitch + q * kLdFPitch, probes + q * D + c,
+                       static_cast<uint32_t>(len * 8), &full_bar[st]);
+        for (int b = 0; b < B; ++b)
+          bulk_load_ld(sb + 8 * kLdPPitch + 8 * kLdFPitch + b * kLdFPitch, proj + b * D + c,
+                       static_cast<uint32_t>(len * 8), &full_bar[st]);
+      }
+    }
+    return;
+  }
+  const int w = warp - 1, g = lane >> 2, k = lane & 3;
+  double acc[8][2];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) acc[q][0] = acc[q][1] = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const int st = i % kLdStages;
+    const long c = d0 + static_cast<long>(i) * kLdChunk;
+    const int len = static_cast<int>(d1 - c < kLdChunk ? d1 - c : kLdChunk);
+    mbar_wait(&full_bar[st], (i / kLdStages) & 1);
+    const uint8_t* sb = smem + st * kLdStage;
+    const __nv_bfloat16* pr = reinterpret_cast<const __nv_bfloat16*>(sb + g * kLdPPitch);
+    const double* qs = reinterpret_cast<const double*>(sb + 8 * kLdPPitch);
+    const double* rr = reinterpret_cast<const double*>(sb + 8 * kLdPPitch + 8 * kLdFPitch + g * kLdFPitch);
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      const int dd = w * 32 + ks * 4 + k;
+      const bool in = dd < len;  // stale data past the chunk end is masked by a = 0
+      const double a = in ? static_cast<double>(__bfloat162float(pr[dd])) : 0.0;
+      const double r = rr[dd];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const double bq = qs[q * (kLdFPitch / 8) + dd] * r;
+        dmma_8x8x4(acc[q], a, bq);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[st]);
+  }
+  // lane holds logits_q[e = g][b = 2k, 2k+1]; warps summed in order
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    red[(w * 8 + q) * 64 + g * 8 + 2 * k] = acc[q][0];
+    red[(w * 8 + q) * 64 + g * 8 + 2 * k + 1] = acc[q][1];
+  }
+  asm volatile("bar.sync 1, 256;" ::: "memory");
+  for (int t = threadIdx.x - 32; t < 8 * 64; t += 256) {
+    const int q = t >> 6, e = (t >> 3) & 7, b = t & 7;
+    if (q < n_probes && e < E && b < B) {
+      double v = 0.0;
+      for (int ww = 0; ww < 8; ++ww) v += red[(ww * 8 + q) * 64 + e * 8 + b];
+      partial[(static_cast<long>(blockIdx.x) * E + e) * n_probes * B + q * B + b] = v;
+    }
+  }
+}
+
 // out[i] = sum over splits (in order) of partial[split][i]; one warp per entry
 __global__ void sim_sum_partials(const double* __restrict__ partial, int splits, long n,
                                  double* __restrict__ out) {
@@ -893,6 +1018,15 @@ static bool sim_logits_small(int E, int buckets, long D) {
   return E <= kLogitE && buckets <= kLogitB && D % 8 == 0;
 }
 
+// fp64 tensor-core surrogate logits (COMOE_SIM_DMMA=0: the vector kernel)
+static bool sim_logits_dmma() {
+  static const bool on = [] {
+    const char* e = std::getenv("COMOE_SIM_DMMA");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // (d per block, blocks) of the small-logit kernel: one block per SM (register-bound)
 static std::pair<long, int> logit_plan(long D) {
   long blocks = static_cast<long>(num_sms());
@@ -1088,7 +1222,16 @@ int comoe_sim_contract(int dtype, const void* const* rows, int E, long D, const 
   const std::pair<long, int> lp = logit_plan(D);
   double* lpart = partial + (comoe_sim_workspace_bytes(E, n_probes, buckets, D) / sizeof(double) -
                              static_cast<long>(lp.second) * E * n_probes * buckets);
-  if (dtype == COMOE_DTYPE_BF16) {
+  if (dtype == COMOE_DTYPE_BF16 && n_probes <= 8 && sim_logits_dmma()) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(sim_logits_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kLdSmem);
+      attr = true;
+    }
+    sim_logits_dmma_kernel<<<lp.second, kLdThreads, kLdSmem, s>>>(rows, E, D, probes, n_probes,
+                                                                  proj, buckets, lp.first, lpart);
+  } else if (dtype == COMOE_DTYPE_BF16) {
     constexpr int smem = 2 * LogitStage<__nv_bfloat16>::kBytes;
     cudaFuncSetAttribute(sim_logits_small_kernel<__nv_bfloat16>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -262,3 +262,20 @@ def test_similarity_cosine_edge_shapes(E, D):
         np.testing.assert_allclose(gram.cpu().numpy(), Go, rtol=1e-6, atol=3e-8 * np.abs(G).max())
         np.testing.assert_allclose(sim.cpu().numpy(), M.cosine_matrix(Vh[order]), rtol=1e-7,
                                    atol=1e-7)
+
+
+@pytest.mark.parametrize("E,n,B,D", [(8, 8, 8, 4096 + 8), (5, 3, 6, 1000), (2, 8, 1, 256 * 7)])
+def test_surrogate_logits_bf16_paths(E, n, B, D):
+    """Surrogate logits of bf16 experts (fp64 tensor-core path, and the
+    vector path under COMOE_SIM_DMMA=0 in CI runs that set it) vs an fp64
+    einsum of the same values: ragged chunks, fewer experts / probes /
+    buckets than the 8x8x8 tile."""
+    from paper_2508_09208_b200 import kernels
+    g = torch.Generator(device="cuda").manual_seed(E * 100 + n * 10 + B)
+    V = (torch.randn(E, D, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+    probes = torch.randn(n, D, device="cuda", generator=g, dtype=torch.float64)
+    proj = torch.randn(B, D, device="cuda", generator=g, dtype=torch.float64)
+    _, _, logits = kernels.similarity([V[e] for e in range(E)], probes, proj, 0.5)
+    P = V.double().cpu().numpy()
+    ref = np.einsum("ed,nd,bd->enb", P, probes.cpu().numpy(), proj.cpu().numpy())
+    np.testing.assert_allclose(logits.cpu().numpy(), ref, rtol=1e-10, atol=1e-12 * np.abs(ref).max())
