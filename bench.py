@@ -301,6 +301,18 @@ def run_ours(args):
                 "peak_source": peak_src,
                 "algorithmic": f"2*kept_rows*d*d_ff = {flops:.4g} FLOP per launch (kept_rows={rows})",
                 "traffic": prof.get(f"{dom}_dram_bytes_per_launch")}
+    # the roof this kernel actually presses on: operand bytes each
+    # SM ingests from L2 per launch (ncu, committed) over the live launch time,
+    # against the measured per-SM ingest ceiling (scripts/l2_probe.cu)
+    ingest = prof.get(f"{dom}_sm_ingest_bytes_per_launch")
+    if ingest and stages.get(dom):
+        per_sm = ingest / 148 / (stages[dom] * 1e-3) / 1e9
+        roofline["sm_ingest"] = {"achieved_GBps_per_sm": per_sm, "ceiling_GBps_per_sm": 105.0,
+                                 "frac": per_sm / 105.0, "bytes_per_launch": ingest,
+                                 "ceiling_source": "profiles/r1_l2_probe.jsonl (15.5 TB/s / 148 SMs)",
+                                 "note": "ceiling = 53 B/clk per SM measured at 1965 MHz; the GEMM "
+                                         "runs power-capped (ncu: ~1.5 GHz), where the same "
+                                         "53 B/clk is ~80 GB/s per SM"}
 
     # ------------------------------------------------ end-to-end (host buffers)
     # Public host-to-host call: HostPipeline streams pinned host batches through
