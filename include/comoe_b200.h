@@ -226,6 +226,10 @@ int comoe_predictor_mlp(const int* slots, int B, int K, const double* emb, int e
                         int hidden, const double* w2, const double* b2, int E, double* probs,
                         double* demand, int demand_mode, void* work, void* stream);
 
+/* dev: {clock64, ns} at the start and end of CTA 0 of the last 2-SM grouped
+ * GEMM launched with COMOE_GEMM_DEBUG bit 256 — the SM clock under load */
+int comoe_debug_gemm_clock(unsigned long long* out4);
+
 #ifdef __cplusplus
 }
 #endif

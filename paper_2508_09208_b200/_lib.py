@@ -38,6 +38,7 @@ _SIGNATURES = {
     "comoe_grouped_ffn": [_p, _c_long, _c_int, _c_int, _c_int, _p, _c_int, _c_long, _p, _p,
                           _p, _c_int, _p, _p, _c_int, _p, _p, _p],
     "comoe_combine": [_p, _p, _p, _c_int, _c_int, _c_int, _p, _p],
+    "comoe_debug_gemm_clock": [_p],
     "comoe_permute_peers": [_p, _c_int, _c_int, _c_int, _p, _p, _p, _p, _p, _c_int, _c_int, _p,
                             _c_int, _c_long, _c_int, _p, _p, _p, _p],
     "comoe_combine_peers": [_p, _c_int, _c_long, _c_int, _p, _p, _c_int, _c_int, _c_int, _p, _p],

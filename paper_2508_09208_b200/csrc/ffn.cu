@@ -227,4 +227,14 @@ int comoe_grouped_ffn(const void* x_perm, long total_rows, int d, int d_ff, int 
                            group_slot, G, mode2, out, ldo, row_token, row_prob, s);
 }
 
+// dev: {clock64, ns} at start and end of CTA 0 of the last 2-SM grouped GEMM
+// launched with COMOE_GEMM_DEBUG bit 256 (synchronises)
+int comoe_debug_gemm_clock(unsigned long long* out4) {
+  using namespace comoe;
+  COMOE_REQUIRE(out4, kBadArg, "debug_gemm_clock: null pointer");
+  const cudaError_t e = cudaMemcpyFromSymbol(out4, g_gemm_clock, sizeof(unsigned long long) * 4);
+  COMOE_REQUIRE(e == cudaSuccess, kCudaError, "debug_gemm_clock: %s", cudaGetErrorString(e));
+  return kOk;
+}
+
 }  // extern "C"

@@ -149,6 +149,8 @@ __device__ __forceinline__ void build_tile_prefix_2sm(const int* __restrict__ ro
   __syncthreads();
 }
 
+static __device__ unsigned long long g_gemm_clock[4];  // dev clock probe (debug bit 256)
+
 struct Tile2 {
   int g, ft, tok0, ntok, nmma;
 };
@@ -230,6 +232,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int total_tiles = prefix[p.G];
+  // dev: SM clock during the launch (COMOE_GEMM_DEBUG bit 256): CTA 0 stamps
+  // clock64 and the global ns timer at start and end (comoe_debug_gemm_clock)
+  if ((p.debug & 256) && blockIdx.x == 0 && threadIdx.x == 0) {
+    g_gemm_clock[0] = clock64();
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_gemm_clock[1]));
+  }
 
   if (warp == 0) {
     // ---------------------------------------------- TMA producer (both CTAs)
@@ -427,6 +435,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base)
                  : "memory");
+  }
+  if ((p.debug & 256) && blockIdx.x == 0 && threadIdx.x == 0) {
+    g_gemm_clock[2] = clock64();
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_gemm_clock[3]));
   }
 }
 
