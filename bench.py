@@ -310,9 +310,10 @@ def run_ours(args):
         roofline["sm_ingest"] = {"achieved_GBps_per_sm": per_sm, "ceiling_GBps_per_sm": 105.0,
                                  "frac": per_sm / 105.0, "bytes_per_launch": ingest,
                                  "ceiling_source": "profiles/r1_l2_probe.jsonl (15.5 TB/s / 148 SMs)",
-                                 "note": "ceiling = 53 B/clk per SM measured at 1965 MHz; the GEMM "
-                                         "runs power-capped (ncu: ~1.5 GHz), where the same "
-                                         "53 B/clk is ~80 GB/s per SM"}
+                                 "note": "ceiling measured with bulk copies at idle clocks; it does "
+                                         "not scale down with the SM clock, while the GEMM itself "
+                                         "runs power-capped at ~1.25 GHz "
+                                         "(profiles/r1_gemm_clock.jsonl)"}
 
     # ------------------------------------------------ end-to-end (host buffers)
     # Public host-to-host call: HostPipeline streams pinned host batches through
