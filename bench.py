@@ -301,6 +301,12 @@ def run_ours(args):
                 "peak_source": peak_src,
                 "algorithmic": f"2*kept_rows*d*d_ff = {flops:.4g} FLOP per launch (kept_rows={rows})",
                 "traffic": prof.get(f"{dom}_dram_bytes_per_launch")}
+    sustained = peaks.get("bf16_tflops_sustained")
+    if sustained and achieved is not None:
+        # the GEMMs run power-capped inside the step loop (~1.25 GHz measured in
+        # the kernel, profiles/r1_gemm_clock.jsonl), the sustained regime
+        roofline["frac_vs_sustained_peak"] = achieved / sustained
+        roofline["sustained_peak"] = sustained
     # the roof this kernel actually presses on: operand bytes each
     # SM ingests from L2 per launch (ncu, committed) over the live launch time,
     # against the measured per-SM ingest ceiling (scripts/l2_probe.cu)
