@@ -27,13 +27,13 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const Group
   return check_launch("grouped_gemm_kernel");
 }
 
-template <int kMode, int kStages, int kEpiWarps>
+template <int kMode, int kStages, int kEpiWarps, int kBN = 256>
 static int launch_gemm_2sm_cfg(const CUtensorMap& tw, const CUtensorMap& tx,
                                const CUtensorMap& to, const GroupedGemmParams& p,
                                cudaStream_t stream) {
-  using C = Gemm2Cfg<kStages, kEpiWarps>;
+  using C = Gemm2Cfg<kStages, kEpiWarps, kBN>;
   if (p.gather_rows) {
-    if constexpr (kMode == kEpiRelu) {
+    if constexpr (kMode == kEpiRelu && kBN == 256) {
       auto kg = grouped_gemm_2sm_kernel<kMode, kStages, kEpiWarps, true>;
       static bool attr_g = false;
       if (!attr_g) {
@@ -49,7 +49,7 @@ static int launch_gemm_2sm_cfg(const CUtensorMap& tw, const CUtensorMap& tx,
     set_error("grouped_gemm: row gather is only supported with the ReLU epilogue");
     return kUnsupportedShape;
   }
-  auto kern = grouped_gemm_2sm_kernel<kMode, kStages, kEpiWarps>;
+  auto kern = grouped_gemm_2sm_kernel<kMode, kStages, kEpiWarps, false, kBN>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kTotal);
@@ -90,6 +90,25 @@ static int launch_gemm_2sm(const CUtensorMap& tw, const CUtensorMap& tx, const C
     case 1: return launch_gemm_2sm_cfg<kMode, 4, 8>(tw, tx, to, p, stream);
     default: return launch_gemm_2sm_cfg<kMode, 6, 4>(tw, tx, to, p, stream);
   }
+}
+
+// Decode-sized batches (a few tokens per expert): 32-token tiles with
+// 16-row token boxes leave room for 10 weight stages (the weight stream,
+// first-touch from HBM, is the whole cost there). COMOE_GEMM_SMALLN=0 off.
+constexpr int kSmallBN = 32;
+static bool small_tiles(long a_rows, int G) {
+  static const bool on = [] {
+    const char* e = std::getenv("COMOE_GEMM_SMALLN");
+    return !(e && e[0] == '0');
+  }();
+  return on && a_rows <= 8L * G;
+}
+
+template <int kMode>
+static int launch_gemm_2sm_small(const CUtensorMap& tw, const CUtensorMap& tx,
+                                 const CUtensorMap& to, const GroupedGemmParams& p,
+                                 cudaStream_t stream) {
+  return launch_gemm_2sm_cfg<kMode, 10, 4, kSmallBN>(tw, tx, to, p, stream);
 }
 
 static int gemm_debug() {
@@ -156,7 +175,9 @@ static int grouped_gemm_impl(const void* a, long a_rows, const void* pool, int n
     // 2-SM swap-AB kernel: weights = A (128-feature boxes), tokens = B (128-row boxes)
     rc = make_tmap_bf16_3d(&tb, b, n_slots, N, K, slot_stride, 128);
     if (rc) return rc;
-    rc = make_tmap_bf16_2d(&ta, a, static_cast<uint64_t>(a_rows), K, a_gather ? 1 : 128);
+    const bool small = !a_gather && small_tiles(a_rows, G);
+    rc = make_tmap_bf16_2d(&ta, a, static_cast<uint64_t>(a_rows), K,
+                           a_gather ? 1 : (small ? kSmallBN / 2 : 128));
     if (rc) return rc;
     // output map for the bulk-store epilogue: [a_rows, N] bf16 at ld ldo, box
     // 32 features x 32 tokens, 64-byte swizzle (unused by the scatter mode)
@@ -164,6 +185,14 @@ static int grouped_gemm_impl(const void* a, long a_rows, const void* pool, int n
     rc = make_tmap_bf16_2d_box(&to, out, static_cast<uint64_t>(a_rows), static_cast<uint64_t>(N),
                                static_cast<uint64_t>(ldo), 32, 32, 64);
     if (rc) return rc;
+    if (small) {
+      switch (epi_mode) {
+        case kEpiRelu: return launch_gemm_2sm_small<kEpiRelu>(tb, ta, to, p, stream);
+        case kEpiScaleScatter: return launch_gemm_2sm_small<kEpiScaleScatter>(tb, ta, to, p, stream);
+        case kEpiStore: return launch_gemm_2sm_small<kEpiStore>(tb, ta, to, p, stream);
+        default: break;
+      }
+    }
     switch (epi_mode) {
       case kEpiRelu: return launch_gemm_2sm<kEpiRelu>(tb, ta, to, p, stream);
       case kEpiScaleScatter: return launch_gemm_2sm<kEpiScaleScatter>(tb, ta, to, p, stream);

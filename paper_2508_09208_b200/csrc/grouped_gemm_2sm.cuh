@@ -29,11 +29,13 @@ constexpr int k2MaxThreads = 128 + 32 * 8;
 // (K3): 512-token tiles sharing each weight stage between two
 // MMAs, dynamic tile claiming through a cross-CTA tile-id ring, split
 // weight/token rings, and L2 prefetch of weight boxes.
-template <int kStages, int kEpiWarps>
+// kBN: tokens per tile (256; 32 for decode-sized batches: 16-row token boxes,
+// so more of the shared memory holds weight stages)
+template <int kStages, int kEpiWarps, int kBN = 256>
 struct Gemm2Cfg {
   static constexpr int kThreads = 128 + 32 * kEpiWarps;  // w0 TMA, w1 MMA, w2 TMEM, w3 idle
   static constexpr int kABytes = 128 * kGemmBK * 2;     // 128 feature rows x 64 K
-  static constexpr int kBBytes = 128 * kGemmBK * 2;     // up to 128 token rows x 64 K
+  static constexpr int kBBytes = (kBN / 2) * kGemmBK * 2;  // up to kBN/2 token rows x 64 K
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTileBytes = kStages * kStageBytes;
   static constexpr int kXposeBytes = 0;                          // (register transpose)
@@ -117,6 +119,7 @@ __device__ __forceinline__ void umma_commit_2sm_mc(uint64_t* bar) {
 }
 
 // tiles of a group: ceil(rows/256) token tiles x (N/256) feature tiles
+template <int kBN>
 __device__ __forceinline__ void build_tile_prefix_2sm(const int* __restrict__ rows, int G,
                                                       int f_tiles, int* prefix) {
   __shared__ int warp_tot2[k2MaxThreads / 32];
@@ -126,7 +129,7 @@ __device__ __forceinline__ void build_tile_prefix_2sm(const int* __restrict__ ro
   const int g0 = tid * per;
   int local = 0;
   for (int i = 0; i < per; ++i)
-    if (g0 + i < G) local += ((__ldg(rows + g0 + i) + k2BN - 1) / k2BN) * f_tiles;
+    if (g0 + i < G) local += ((__ldg(rows + g0 + i) + kBN - 1) / kBN) * f_tiles;
   int v = local;
   const int lane = tid & 31, w = tid >> 5;
 #pragma unroll
@@ -142,7 +145,7 @@ __device__ __forceinline__ void build_tile_prefix_2sm(const int* __restrict__ ro
     const int g = g0 + i;
     if (g < G) {
       prefix[g] = run;
-      run += ((__ldg(rows + g) + k2BN - 1) / k2BN) * f_tiles;
+      run += ((__ldg(rows + g) + kBN - 1) / kBN) * f_tiles;
     }
   }
   if (tid == nthreads - 1) prefix[G] = run;
@@ -155,6 +158,7 @@ struct Tile2 {
   int g, ft, tok0, ntok, nmma;
 };
 
+template <int kBN>
 __device__ __forceinline__ Tile2 decode_tile2(const int* prefix, const GroupedGemmParams& p,
                                               int f_tiles, int tile) {
   Tile2 t;
@@ -163,26 +167,27 @@ __device__ __forceinline__ Tile2 decode_tile2(const int* prefix, const GroupedGe
   const int rows = __ldg(p.group_rows + t.g);
   int tt;
   if (p.ft_major) {  // big weight blocks: neighbouring pairs share a weight tile
-    const int n_tt = (rows + k2BN - 1) / k2BN;
+    const int n_tt = (rows + kBN - 1) / kBN;
     tt = local % n_tt;
     t.ft = local / n_tt;
   } else {
     tt = local / f_tiles;
     t.ft = local % f_tiles;
   }
-  t.tok0 = tt * k2BN;
-  t.ntok = min(k2BN, rows - t.tok0);
+  t.tok0 = tt * kBN;
+  t.ntok = min(kBN, rows - t.tok0);
   t.nmma = (t.ntok + 15) & ~15;
   return t;
 }
 
-template <int kMode, int k2Stages, int k2EpiWarps, bool kGather = false>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k2EpiWarps>::kThreads, 1)
+template <int kMode, int k2Stages, int k2EpiWarps, bool kGather = false, int kBN = 256>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k2EpiWarps, kBN>::kThreads, 1)
     grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmap_w,
                             const __grid_constant__ CUtensorMap tmap_x,
                             const __grid_constant__ CUtensorMap tmap_out, GroupedGemmParams p) {
   static_assert(kMode != kEpiSwiGLU, "SwiGLU uses the 1-SM kernel");
-  using S = Gemm2Cfg<k2Stages, k2EpiWarps>;
+  using S = Gemm2Cfg<k2Stages, k2EpiWarps, kBN>;
+  static_assert(!kGather || kBN == 256, "the token gather fills 128-row boxes");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -226,7 +231,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k
   }
   pdl_wait();     // group tables / token rows come from the preceding kernels
   pdl_trigger();  // persistent grid: the next kernel may launch and wait
-  build_tile_prefix_2sm(p.group_rows, p.G, f_tiles, prefix);
+  build_tile_prefix_2sm<kBN>(p.group_rows, p.G, f_tiles, prefix);
   tc_fence_before();
   cluster_sync_all();
   tc_fence_after();
@@ -248,7 +253,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k
     int stage = 0;
     uint32_t phase = 0;
     for (int tile = cluster; tile < total_tiles; tile += n_clusters) {
-      const Tile2 t = decode_tile2(prefix, p, f_tiles, tile);
+      const Tile2 t = decode_tile2<kBN>(prefix, p, f_tiles, tile);
       // (dev attribution: debug 16 = every tile loads slot 0 and token row 0,
       // 128 = slot 0 only — L2-resident operands; +27-42% / +17% at C2)
       const int slot = (p.debug & (16 | 128)) ? 0 : __ldg(p.group_slot + t.g);
@@ -299,12 +304,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k
       uint32_t phase = 0;
       int it = 0;
       for (int tile = cluster; tile < total_tiles; tile += n_clusters, ++it) {
-        const Tile2 t = decode_tile2(prefix, p, f_tiles, tile);
+        const Tile2 t = decode_tile2<kBN>(prefix, p, f_tiles, tile);
         const uint32_t idesc = umma_idesc_bf16_f32(k2BM, t.nmma);
         const int acc = it & 1;
         mbar_wait(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * k2BN;
+        const uint32_t d_tmem = tmem_base + acc * kBN;
         for (int kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
@@ -334,13 +339,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k
     int nbuf = 0;
     int it = 0;
     for (int tile = cluster; tile < total_tiles; tile += n_clusters, ++it) {
-      const Tile2 t = decode_tile2(prefix, p, f_tiles, tile);
+      const Tile2 t = decode_tile2<kBN>(prefix, p, f_tiles, tile);
       const int acc = it & 1;
       const long row_base = static_cast<long>(__ldg(p.group_row_base + t.g)) + t.tok0;
       const long col0 = static_cast<long>(t.ft) * k2BM + rank * 128 + q * 32;
       mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
       tc_fence_after();
-      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * k2BN;
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * kBN;
       const int chunks = (t.nmma + 31) >> 5;
       bool released = false;
       for (int ci = sub; ci < chunks; ci += kSubs) {
