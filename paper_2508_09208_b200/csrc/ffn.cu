@@ -95,20 +95,30 @@ static int launch_gemm_2sm(const CUtensorMap& tw, const CUtensorMap& tx, const C
 // Decode-sized batches (a few tokens per expert): 32-token tiles with
 // 16-row token boxes leave room for 10 weight stages (the weight stream,
 // first-touch from HBM, is the whole cost there). COMOE_GEMM_SMALLN=0 off.
-constexpr int kSmallBN = 32;
-static bool small_tiles(long a_rows, int G) {
-  static const bool on = [] {
+// COMOE_GEMM_SMALLN: 0 = 256-token tiles only, 1 = + 32-token tiles, 2
+// (default) = + 64-token tiles with 9 stages up to 32 rows per group
+// (4096 tokens over 128 experts: 239 -> 233 us per layer)
+static int small_mode() {
+  static const int m = [] {
     const char* e = std::getenv("COMOE_GEMM_SMALLN");
-    return !(e && e[0] == '0');
+    return e ? std::atoi(e) : 2;
   }();
-  return on && a_rows <= 8L * G;
+  return m;
+}
+// token rows per tile: 32 (<= 8 rows per group on average), 64 (mode 2, <= 32), else 256
+static int tile_tokens(long a_rows, int G) {
+  const int m = small_mode();
+  if (m >= 1 && a_rows <= 8L * G) return 32;
+  if (m >= 2 && a_rows <= 32L * G) return 64;
+  return 256;
 }
 
 template <int kMode>
 static int launch_gemm_2sm_small(const CUtensorMap& tw, const CUtensorMap& tx,
-                                 const CUtensorMap& to, const GroupedGemmParams& p,
+                                 const CUtensorMap& to, const GroupedGemmParams& p, int bn,
                                  cudaStream_t stream) {
-  return launch_gemm_2sm_cfg<kMode, 10, 4, kSmallBN>(tw, tx, to, p, stream);
+  if (bn == 64) return launch_gemm_2sm_cfg<kMode, 9, 4, 64>(tw, tx, to, p, stream);
+  return launch_gemm_2sm_cfg<kMode, 10, 4, 32>(tw, tx, to, p, stream);
 }
 
 static int gemm_debug() {
@@ -175,9 +185,9 @@ static int grouped_gemm_impl(const void* a, long a_rows, const void* pool, int n
     // 2-SM swap-AB kernel: weights = A (128-feature boxes), tokens = B (128-row boxes)
     rc = make_tmap_bf16_3d(&tb, b, n_slots, N, K, slot_stride, 128);
     if (rc) return rc;
-    const bool small = !a_gather && small_tiles(a_rows, G);
-    rc = make_tmap_bf16_2d(&ta, a, static_cast<uint64_t>(a_rows), K,
-                           a_gather ? 1 : (small ? kSmallBN / 2 : 128));
+    const int bn = a_gather ? 256 : tile_tokens(a_rows, G);
+    const bool small = bn < 256;
+    rc = make_tmap_bf16_2d(&ta, a, static_cast<uint64_t>(a_rows), K, a_gather ? 1 : bn / 2);
     if (rc) return rc;
     // output map for the bulk-store epilogue: [a_rows, N] bf16 at ld ldo, box
     // 32 features x 32 tokens, 64-byte swizzle (unused by the scatter mode)
@@ -187,9 +197,9 @@ static int grouped_gemm_impl(const void* a, long a_rows, const void* pool, int n
     if (rc) return rc;
     if (small) {
       switch (epi_mode) {
-        case kEpiRelu: return launch_gemm_2sm_small<kEpiRelu>(tb, ta, to, p, stream);
-        case kEpiScaleScatter: return launch_gemm_2sm_small<kEpiScaleScatter>(tb, ta, to, p, stream);
-        case kEpiStore: return launch_gemm_2sm_small<kEpiStore>(tb, ta, to, p, stream);
+        case kEpiRelu: return launch_gemm_2sm_small<kEpiRelu>(tb, ta, to, p, bn, stream);
+        case kEpiScaleScatter: return launch_gemm_2sm_small<kEpiScaleScatter>(tb, ta, to, p, bn, stream);
+        case kEpiStore: return launch_gemm_2sm_small<kEpiStore>(tb, ta, to, p, bn, stream);
         default: break;
       }
     }
