@@ -33,8 +33,8 @@ import torch
 
 from . import kernels
 from .errors import InfeasibleError
-from .layer import ACTS, MoELayer
-from .offload import (CACHE, HOST, WORKSPACE, CacheState, OffloadPolicy, build_cache_state,
+from .layer import MoELayer
+from .offload import (CACHE, HOST, WORKSPACE, OffloadPolicy, build_cache_state,
                       correct_misprediction, decide_prefetch, eviction_score, evict,
                       plan_initial_placement)
 from .pool import ExpertPool
