@@ -168,6 +168,13 @@ __global__ void __launch_bounds__(kGateThreads, 1)
       2 * kAccCols <= 32 ? 32 : (2 * kAccCols <= 64 ? 64 : (2 * kAccCols <= 128 ? 128 : (2 * kAccCols <= 256 ? 256 : 512)));
   constexpr uint32_t kIdesc = umma_idesc_bf16_f32(kPair ? 256 : kGemmBM, kAccCols);
   constexpr int kBRows = S::kBRows;
+  // kSplitEpi: both epilogue groups work on every unit, each on half of the
+  // experts of the same tokens (warps 4+q and 8+q share TMEM lane quarter q);
+  // group 1 hands its partial top-2 / softmax sum to group 0 through shared
+  // memory and group 0 finishes. Halves each unit's epilogue latency, which
+  // set the tail of the MMA -> epilogue chain (the alternating-groups form
+  // left one full epilogue after the last MMA).
+  constexpr bool kSplitEpi = kCat && EP >= 32;
   if (p.debug & 32) return;  // dev: empty launch
 
   extern __shared__ uint8_t smem_raw[];
@@ -203,7 +210,7 @@ __global__ void __launch_bounds__(kGateThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], kPair ? 8 : 4);
+      mbar_init(&tempty_bar[a], kPair ? (kSplitEpi ? 16 : 8) : 4);
     }
     fence_barrier_init();
   }
@@ -305,6 +312,174 @@ __global__ void __launch_bounds__(kGateThreads, 1)
         if constexpr (kPair) umma_commit_2sm_mc(&tfull_bar[acc]);
         else umma_commit(&tfull_bar[acc]);
       }
+    }
+  } else if (kSplitEpi && warp >= 4) {
+    const int q = warp & 3;
+    const int half = (warp - 4) >> 2;  // 0: experts [0, EP/2) and the finish; 1: [EP/2, EP)
+    const int et = threadIdx.x - 128;  // 0..127 in group 0
+    int* cnt = cnt_all;
+    // group 1's counters are unused here: they hold the hand-off [128 tokens][6]
+    uint32_t* xch = reinterpret_cast<uint32_t*>(cnt_all + kGateMaxK * 4 * kGateMaxE);
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    constexpr int kHalf = EP / 2;
+    constexpr int kChunks = kHalf / 16;
+    constexpr float kLog2e = 1.4426950408889634f;
+    const bool need_sum = !p.norm_topk;
+    int it = 0;
+    for (int u = unit0; u < n_units; u += unit_step, ++it) {
+      const int acc = it & 1;
+      const int tile = 2 * u + static_cast<int>(rank);
+      const bool tile_ok = tile < p.ntiles;
+      const int t = tile * kGemmBM + q * 32 + lane;
+      const bool valid = tile_ok && t < p.T;
+      mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const int e0 = half * kHalf;
+      const uint32_t t_row =
+          tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * kAccCols + e0;
+      GateTop2 ta, tb;
+      float m = -INFINITY, s4[2] = {0.f, 0.f};
+      float* lrow = (p.logits && valid) ? p.logits + static_cast<long>(t) * p.E : nullptr;
+      uint32_t buf[2][32];
+      gate_ld_chunk<true, EP>(t_row, buf[0]);
+#pragma unroll
+      for (int c = 0; c < kChunks; ++c) {
+        uint32_t(&cur)[32] = buf[c & 1];
+        gate_ld_wait<true>(cur);
+        if (c + 1 < kChunks) {
+          gate_ld_chunk<true, EP>(t_row + (c + 1) * 16, buf[(c + 1) & 1]);
+        } else {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(smem_u32(&tempty_bar[acc]) & kPeerMask);
+        }
+        float v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int e = e0 + c * 16 + j;
+          const float x = __uint_as_float(cur[j]) + __uint_as_float(cur[16 + j]);
+          v[j] = e < p.E ? x : -INFINITY;
+        }
+#pragma unroll
+        for (int j = 0; j < 16; j += 2) {
+          ta.push(v[j], e0 + c * 16 + j);
+          tb.push(v[j + 1], e0 + c * 16 + j + 1);
+        }
+        if (lrow) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (e0 + c * 16 + j < p.E) lrow[e0 + c * 16 + j] = v[j];
+        }
+        if (need_sum) {
+          const float mn = fmaxf(m, fmaxf(ta.v1, tb.v1));
+          const float mb = mn * kLog2e;
+          const float sc = m == -INFINITY ? 0.f : ex2_approx((m - mn) * kLog2e);
+          s4[0] *= sc;
+          s4[1] *= sc;
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            s4[j & 1] += (mn == -INFINITY) ? 0.f : ex2_approx(fmaf(v[j], kLog2e, -mb));
+          m = mn;
+        }
+      }
+      float v1, v2;
+      int i1, i2;
+      gate_top2_merge(ta, tb, v1, i1, v2, i2);
+      float s = s4[0] + s4[1];
+      uint32_t* slot = xch + (q * 32 + lane) * 6;
+      if (half == 1) {
+        slot[0] = __float_as_uint(v1);
+        slot[1] = static_cast<uint32_t>(i1);
+        slot[2] = __float_as_uint(v2);
+        slot[3] = static_cast<uint32_t>(i2);
+        slot[4] = __float_as_uint(m);
+        slot[5] = __float_as_uint(s);
+      }
+      named_bar_sync(3 + q, 64);  // half 1's partials are in shared memory
+      if (half == 1) {
+        named_bar_sync(7 + q, 64);  // group 0 has read them
+        continue;
+      }
+      GateTop2 a0, a1;
+      a0.v1 = v1; a0.i1 = i1; a0.v2 = v2; a0.i2 = i2;
+      a1.v1 = __uint_as_float(slot[0]);
+      a1.i1 = static_cast<int>(slot[1]);
+      a1.v2 = __uint_as_float(slot[2]);
+      a1.i2 = static_cast<int>(slot[3]);
+      const float m1 = __uint_as_float(slot[4]), s1 = __uint_as_float(slot[5]);
+      named_bar_sync(7 + q, 64);
+      gate_top2_merge(a0, a1, v1, i1, v2, i2);  // expert ids of half 0 are all lower
+      if (need_sum) {
+        const float mt = fmaxf(m, m1);
+        s = (m == -INFINITY ? 0.f : s * ex2_approx((m - mt) * kLog2e)) +
+            (m1 == -INFINITY ? 0.f : s1 * ex2_approx((m1 - mt) * kLog2e));
+      } else {
+        s = 1.f;
+      }
+
+      float pr0, pr1 = 0.f;
+      if (p.top_k == 1) {
+        pr0 = p.norm_topk ? 1.f : 1.f / s;
+      } else if (p.norm_topk) {
+        const float z = expf(v2 - v1);
+        pr0 = 1.f / (1.f + z);
+        pr1 = z / (1.f + z);
+      } else {
+        pr0 = 1.f / s;
+        pr1 = expf(v2 - v1) / s;
+      }
+      int gr0 = (valid && i1 >= 0) ? smap[i1] : -1;
+      int gr1 = (valid && p.top_k == 2 && i2 >= 0) ? smap[i2] : -1;
+      if (gr1 >= 0 && gr1 == gr0) {
+        pr0 += pr1;
+        pr1 = 0.f;
+        gr1 = -1;
+      }
+      named_bar_sync(1, 128);
+      for (int i = et; i < p.top_k * 4 * kGateMaxE; i += 128) cnt[i] = 0;
+      named_bar_sync(1, 128);
+      int wr0, wr1 = 0;
+      {
+        const unsigned mm0 = __match_any_sync(0xffffffffu, gr0);
+        wr0 = __popc(mm0 & lt_mask);
+        if (gr0 >= 0 && wr0 == 0) cnt[q * kGateMaxE + gr0] = __popc(mm0);
+        if (p.top_k == 2) {
+          const unsigned mm1 = __match_any_sync(0xffffffffu, gr1);
+          wr1 = __popc(mm1 & lt_mask);
+          if (gr1 >= 0 && wr1 == 0) cnt[(4 + q) * kGateMaxE + gr1] = __popc(mm1);
+        }
+      }
+      named_bar_sync(1, 128);
+      if (valid) {
+        int rank0 = -1, rank1 = -1;
+        if (gr0 >= 0) {
+          rank0 = wr0;
+          for (int qq = 0; qq < q; ++qq) rank0 += cnt[qq * kGateMaxE + gr0];
+        }
+        if (gr1 >= 0) {
+          rank1 = wr1;
+          for (int qq = 0; qq < q; ++qq) rank1 += cnt[(4 + qq) * kGateMaxE + gr1];
+        }
+        const long o = static_cast<long>(t) * p.top_k;
+        p.expert_idx[o] = i1;
+        p.group_idx[o] = gr0;
+        p.gate_prob[o] = gr0 >= 0 ? pr0 : 0.f;
+        p.local_rank[o] = rank0;
+        if (p.top_k == 2) {
+          p.expert_idx[o + 1] = i2;
+          p.group_idx[o + 1] = gr1;
+          p.gate_prob[o + 1] = gr1 >= 0 ? pr1 : 0.f;
+          p.local_rank[o + 1] = rank1;
+        }
+      }
+      if (tile_ok)
+        for (int j = 0; j < p.top_k; ++j)
+          for (int g = et; g < p.G; g += 128) {
+            int h = 0;
+            if (g < kGateMaxE)
+              for (int qq = 0; qq < 4; ++qq) h += cnt[(j * 4 + qq) * kGateMaxE + g];
+            p.tile_hist[(static_cast<long>(j) * p.ntiles + tile) * p.G + g] = h;
+          }
     }
   } else if (warp >= 4) {
     const int q = warp & 3;

@@ -100,25 +100,27 @@ def test_shape_errors_raise_before_launch():
         kernels.gate_padded_experts(129)
 
 
-@pytest.mark.parametrize("top_k", [1, 2])
-def test_logit_ties_pick_lowest_expert(top_k):
+@pytest.mark.parametrize("top_k,E", [(1, 16), (2, 16), (1, 64), (2, 64)])
+def test_logit_ties_pick_lowest_expert(top_k, E):
     """Exactly equal logits (duplicate router columns; all-zero tokens) go to
     the lowest expert id, the reference's tie rule (aggregation.py:165,193),
-    including ties between even and odd expert columns."""
-    layer, x, wg, w = _make(700, 256, 256, 16, 2.0, seed=6, top_k=top_k)
+    including ties between even and odd expert columns and (E = 64, the
+    split epilogue) between the two halves of the experts."""
+    layer, x, wg, w = _make(700, 256, 256, E, 2.0, seed=6, top_k=top_k)
     wg = wg.clone()
     x = x.clone()
     x[:, 0] = 1.0
-    wg[:, 12] = wg[:, 5]
+    far = 12 if E == 16 else 40  # E = 64: a duplicate in the other half
+    wg[:, far] = wg[:, 5]
     wg[:, 2] = wg[:, 5]
-    wg[0, 5] = wg[0, 2] = wg[0, 12] = 40.0  # columns 2, 5, 12 win with equal logits
+    wg[0, 5] = wg[0, 2] = wg[0, far] = 40.0  # three columns win with equal logits
     x[600:] = 0                               # all-zero tokens: every logit is 0
     from paper_2508_09208_b200 import MoELayer
     layer = MoELayer(wg.cuda(), layer.pool, 256, top_k=top_k, capacity_factor=2.0)
     info = _check(layer, x, wg, w, 2.0, top_k=top_k)  # parity with the oracle on device logits
     idx = info["expert_idx"]
     lg = layer.last.gate.logits.cpu().numpy()
-    tied = (lg[:600, 2] == lg[:600, 5]) & (lg[:600, 5] == lg[:600, 12])
+    tied = (lg[:600, 2] == lg[:600, 5]) & (lg[:600, 5] == lg[:600, far])
     assert tied.mean() > 0.9  # identical columns give identical MMA sums
     assert (idx[:600][tied, 0] == 2).all() and (idx[600:, 0] == 0).all()
     if top_k == 2:
