@@ -311,7 +311,7 @@ def run_ours(args):
     # SM ingests from L2 per launch (ncu, committed) over the live launch time,
     # against the measured per-SM ingest ceiling (scripts/l2_probe.cu)
     ingest = prof.get(f"{dom}_sm_ingest_bytes_per_launch")
-    if ingest and stages.get(dom):
+    if ingest and stages.get(dom) and world == 1 and not args.force_ep:  # profiled shape only
         per_sm = ingest / 148 / (stages[dom] * 1e-3) / 1e9
         roofline["sm_ingest"] = {"achieved_GBps_per_sm": per_sm, "ceiling_GBps_per_sm": 105.0,
                                  "frac": per_sm / 105.0, "bytes_per_launch": ingest,
