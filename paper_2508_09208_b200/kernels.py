@@ -412,8 +412,10 @@ def similarity(rows, probes, proj, alpha):
     dt = rows[0].dtype
     if dt not in (torch.bfloat16, torch.float64):
         raise ValueError("similarity supports bf16 and float64 parameters")
+    # the bf16 kernels for D % 8 == 0 move rows in 16-byte vectors / bulk copies
+    row_align = 16 if (dt == torch.bfloat16 and D % 8 == 0) else rows[0].element_size()
     for r in rows:
-        _need(r, "row", dt, align=r.element_size())
+        _need(r, "row", dt, align=row_align)
         if r.numel() != D:
             raise ValueError("parameter dimension mismatch")
     n = 0 if probes is None else probes.shape[0]
