@@ -289,10 +289,11 @@ def run_ours(args):
         kept = int(layer.ops.last_recv_counts.sum().item())  # EP: rows this rank's GEMMs compute
     value = T_PER_GPU * world / (ms * 1e-3)
 
-    # dominant kernel roofline: grouped GEMM (ffn1/ffn2) on the tensor pipe
-    dom = max(("ffn1", "ffn2"), key=lambda k: stages.get(k, 0.0))
+    # dominant kernel roofline: grouped GEMM (ffn1/ffn2) on the tensor pipe,
+    # or the fused FFN (opt-in, COMOE_FUSED_FFN=1: both GEMMs in one launch)
+    dom = max(("ffn1", "ffn2", "ffn"), key=lambda k: stages.get(k, 0.0))
     rows = kept if kept is not None else T_PER_GPU
-    flops = 2.0 * rows * D * D_FF
+    flops = 2.0 * rows * D * D_FF * (2 if dom == "ffn" else 1)
     achieved = flops / (stages[dom] * 1e-3) / 1e12 if stages.get(dom) else None
     prof = _profile_summary() or {}
     roofline = {"bound": "tensor", "kernel": f"grouped_gemm ({dom})", "achieved": achieved,

@@ -19,7 +19,7 @@
 extern "C" {
 #endif
 
-#define COMOE_B200_ABI_VERSION 1
+#define COMOE_B200_ABI_VERSION 2
 
 /* status codes */
 #define COMOE_OK 0
@@ -132,6 +132,27 @@ int comoe_grouped_ffn(const void* x_perm, long total_rows, int d, int d_ff, int 
                       const int* group_row_base, const int* group_slot, int G, void* h_work,
                       void* out, int ldo, const int* row_token, const float* row_prob,
                       void* stream);
+/* comoe_fused_ffn: the whole expert FFN in one launch with H kept on chip
+ * (GEMM1 -> ReLU -> bf16 H in TMEM/shared memory -> GEMM2; no h_work, no
+ * H round trip through HBM). Same group table and output semantics as
+ * comoe_grouped_ffn. If gather_rows != NULL, token row r of the permuted
+ * order is row gather_rows[r] of x (TMA gather4 from the unpermuted tokens,
+ * so no permuted copy is needed; pass the permute kernel's row_token).
+ * ReLU experts with d % 256 == 0, d <= 768, d_ff % 256 == 0, G <= 256
+ * (comoe_fused_ffn_supported says whether a shape qualifies). Opt-in: with
+ * env COMOE_FUSED_FFN=1 (comoe_fused_ffn_enabled() == 1) comoe_grouped_ffn
+ * takes this path by itself for qualifying shapes (h_work may then be NULL);
+ * by default the two-launch FFN runs, which measured faster (K3F).
+ */
+int comoe_fused_ffn(const void* x, long x_rows, const int* gather_rows, int d, int d_ff,
+                    const void* pool, int n_slots, long slot_stride, const int* group_rows,
+                    const int* group_row_base, const int* group_slot, int G, void* out, int ldo,
+                    const int* row_token, const float* row_prob, void* stream);
+int comoe_fused_ffn_supported(int d, int d_ff, int act, int G);
+int comoe_fused_ffn_enabled(void);
+/* dev: per-CTA-pair wait-cycle counters of the last fused FFN launched with
+ * env COMOE_FUSED_DEBUG bit 256 (128 x 16 unsigned long long; synchronises) */
+int comoe_debug_fused_prof(unsigned long long* out);
 
 /* ---------------------------------------------------------------- K4 combine
  * y[t] = sum_j gate_prob[t,j] * y_perm[token_pos[t,j]] (token_pos -1 -> 0).

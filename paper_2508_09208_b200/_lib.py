@@ -13,7 +13,7 @@ import threading
 from pathlib import Path
 
 _LIB_PATH = Path(__file__).resolve().parent / "libcomoe_b200.so"
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 _c_int, _c_long, _c_double = ctypes.c_int, ctypes.c_long, ctypes.c_double
 _p = ctypes.c_void_p
@@ -37,6 +37,11 @@ _SIGNATURES = {
                            _p, _c_int, _c_int, _p, _c_int, _p, _p, _p, _p],
     "comoe_grouped_ffn": [_p, _c_long, _c_int, _c_int, _c_int, _p, _c_int, _c_long, _p, _p,
                           _p, _c_int, _p, _p, _c_int, _p, _p, _p],
+    "comoe_fused_ffn": [_p, _c_long, _p, _c_int, _c_int, _p, _c_int, _c_long, _p, _p, _p, _c_int,
+                        _p, _c_int, _p, _p, _p],
+    "comoe_fused_ffn_supported": [_c_int, _c_int, _c_int, _c_int],
+    "comoe_fused_ffn_enabled": [],
+    "comoe_debug_fused_prof": [_p],
     "comoe_combine": [_p, _p, _p, _c_int, _c_int, _c_int, _p, _p],
     "comoe_debug_gemm_clock": [_p],
     "comoe_permute_peers": [_p, _c_int, _c_int, _c_int, _p, _p, _p, _p, _p, _c_int, _c_int, _p,

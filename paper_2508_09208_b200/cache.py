@@ -352,8 +352,9 @@ class CachedMoELayer:
         comp = torch.cuda.current_stream()
         r = L.route(x, routing=routing)
         k1 = L.top_k == 1
+        fused, gather = ws["fused"], ws["gather"]
         kernels.permute(x, r.gate, r.scan, r.capacity, r.rows, y_zero=out if k1 else None,
-                        out=r.perm)
+                        out=r.perm, copy_rows=not gather)
         kept = r.scan.group_kept.cpu().numpy()  # the demand set (the layer's one host sync)
         if after_route is not None:
             after_route(r)
@@ -385,11 +386,19 @@ class CachedMoELayer:
             self._tables_dev[w].copy_(self._tables[w], non_blocking=True)
             c.wait_ready(used, comp)
             g_rows, g_slot = self._tables_dev[w, 0, :G], self._tables_dev[w, 1, :G]
-            kernels.grouped_gemm(r.perm.x_perm, c.pool.data, 0, n1, g_rows, r.scan.group_base,
-                                 g_slot, epi1, ws["h"])
-            kernels.grouped_gemm(ws["h"], c.pool.data, n1 * L.d, L.d, g_rows, r.scan.group_base,
-                                 g_slot, epi2, dst, row_token=r.perm.row_token if k1 else None,
-                                 row_prob=r.perm.row_prob if k1 else None)
+            if fused:  # K3F over this wave's groups (H on chip)
+                kernels.fused_ffn(x if gather else r.perm.x_perm, c.pool.data, L.d_ff, g_rows,
+                                  r.scan.group_base, g_slot, dst,
+                                  gather_rows=r.perm.row_token if gather else None,
+                                  row_token=r.perm.row_token if k1 else None,
+                                  row_prob=r.perm.row_prob if k1 else None)
+            else:
+                kernels.grouped_gemm(r.perm.x_perm, c.pool.data, 0, n1, g_rows,
+                                     r.scan.group_base, g_slot, epi1, ws["h"])
+                kernels.grouped_gemm(ws["h"], c.pool.data, n1 * L.d, L.d, g_rows,
+                                     r.scan.group_base, g_slot, epi2, dst,
+                                     row_token=r.perm.row_token if k1 else None,
+                                     row_prob=r.perm.row_prob if k1 else None)
             c.mark_used(used, comp)
             c.unpin(list(ids) + [e for e in c.slot_of if c.slot_of[e] in used])
         if not k1:

@@ -115,6 +115,30 @@ int make_tmap_bf16_3d(CUtensorMap* map, const void* base, uint64_t slots, uint64
   return kOk;
 }
 
+int make_tmap_bf16_kblk(CUtensorMap* map, const void* base, uint64_t slots, uint64_t rows,
+                        uint64_t cols, uint64_t slot_stride, uint32_t box_rows,
+                        uint32_t box_kblocks) {
+  std::call_once(g_encode_once, load_encode);
+  COMOE_REQUIRE(g_encode != nullptr, kNoDriver, "cuTensorMapEncodeTiled unavailable (no driver)");
+  COMOE_REQUIRE((reinterpret_cast<uintptr_t>(base) & 15) == 0, kBadArg,
+                "tensor base must be 16-byte aligned");
+  COMOE_REQUIRE(cols % 64 == 0 && rows > 0 && slots > 0 && slot_stride % 8 == 0 &&
+                    slot_stride >= rows * cols && box_kblocks >= 1 && box_kblocks <= cols / 64,
+                kUnsupportedShape, "k-block tensor map %llux%llux%llu unsupported",
+                (unsigned long long)slots, (unsigned long long)rows, (unsigned long long)cols);
+  cuuint64_t dims[4] = {64, rows, cols / 64, slots};
+  cuuint64_t strides[3] = {cols * 2, 128, slot_stride * 2};
+  cuuint32_t box[4] = {64, box_rows, box_kblocks, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  COMOE_REQUIRE(r == CUDA_SUCCESS, kCudaError, "cuTensorMapEncodeTiled(k-block 4d) failed (%d)",
+                (int)r);
+  return kOk;
+}
+
 }  // namespace comoe
 
 extern "C" {

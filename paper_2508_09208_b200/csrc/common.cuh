@@ -58,6 +58,14 @@ int make_tmap_bf16_2d_box(CUtensorMap* map, const void* base, uint64_t rows, uin
 int make_tmap_bf16_3d(CUtensorMap* map, const void* base, uint64_t slots, uint64_t rows,
                       uint64_t cols, uint64_t slot_stride, uint32_t box_rows);
 
+// 4-D bf16 tensor map over the same slot pool, viewing each row as cols/64
+// k-blocks: dims {64, rows, k-block, slot}; a box {64, box_rows, box_kblocks,
+// 1} lands as box_kblocks consecutive [box_rows x 64] K-major 128B-swizzled
+// tiles, i.e. several k-blocks per TMA instruction.
+int make_tmap_bf16_kblk(CUtensorMap* map, const void* base, uint64_t slots, uint64_t rows,
+                        uint64_t cols, uint64_t slot_stride, uint32_t box_rows,
+                        uint32_t box_kblocks);
+
 #ifdef __CUDACC__
 
 // PDL: wait until the preceding grid has completed and its writes are

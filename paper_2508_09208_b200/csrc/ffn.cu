@@ -5,10 +5,98 @@
 // reference's flat `Expert.params` (pkg/src/comoe/moe.py:69-74).
 #include <cstdlib>
 
-#include "grouped_gemm_2sm.cuh"
+#include "fused_ffn.cuh"
 #include "../../include/comoe_b200.h"
 
 namespace comoe {
+
+// ---------------------------------------------------------------- fused FFN
+// Opt-in (COMOE_FUSED_FFN=1): comoe_grouped_ffn then runs the fused kernel
+// for qualifying shapes. Measured slower than the two-launch FFN at every
+// batch size of the C2 layer (K3F: 725 vs 574 us at 65,536 tokens,
+// 317 vs 247 us at 16,384, 189 vs 171 us at 256), so it is not the default.
+static bool fused_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("COMOE_FUSED_FFN");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+static bool fused_supported(int d, int d_ff, int act, int G) {
+  return act == COMOE_ACT_RELU && d > 0 && d % 256 == 0 && d <= kFMaxD && d_ff > 0 &&
+         d_ff % kFChunk == 0 && G >= 1 && G <= kFMaxGroups;
+}
+
+// k-blocks per weight TMA / ring stage (COMOE_FUSED_BOXES: 1 = 6 x 16 KB,
+// 2 = 3 x 32 KB, the default: the single producer thread needs >= 8 MMAs of
+// work per TMA it issues)
+static int fused_boxes() {
+  static const int v = [] {
+    const char* e = std::getenv("COMOE_FUSED_BOXES");
+    return e && std::atoi(e) == 1 ? 1 : 2;
+  }();
+  return v;
+}
+static int fused_debug() {
+  static const int v = [] {
+    const char* e = std::getenv("COMOE_FUSED_DEBUG");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
+template <int kStages, int kBoxes, bool kGather>
+static int launch_fused(const CUtensorMap& twi, const CUtensorMap& two, const CUtensorMap& tx,
+                        const FusedFfnParams& p, cudaStream_t stream) {
+  auto kern = fused_ffn_kernel<kStages, kBoxes, kGather>;
+  const int smem = FusedCfg<kStages, kBoxes>::smem_bytes(p.d);
+  static int attr_set = 0;  // per instantiation: the largest size set so far
+  if (attr_set < smem) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr_set = smem;
+  }
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  kern<<<sms & ~1, kFThreads, smem, stream>>>(twi, two, tx, p);
+  return check_launch("fused_ffn_kernel");
+}
+
+static int fused_ffn_impl(const void* x, long x_rows, const int* gather_rows, int d, int d_ff,
+                          const void* pool, int n_slots, long slot_stride, const int* group_rows,
+                          const int* group_row_base, const int* group_slot, int G, void* out,
+                          int ldo, const int* row_token, const float* row_prob,
+                          cudaStream_t stream) {
+  COMOE_REQUIRE(x && pool && out && group_rows && group_row_base && group_slot, kBadArg,
+                "fused_ffn: null pointer");
+  COMOE_REQUIRE(fused_supported(d, d_ff, COMOE_ACT_RELU, G), kUnsupportedShape,
+                "fused_ffn: d=%d d_ff=%d G=%d unsupported (ReLU, d %% 256 == 0, d <= %d, "
+                "d_ff %% 256 == 0, G <= %d)", d, d_ff, G, kFMaxD, kFMaxGroups);
+  COMOE_REQUIRE(x_rows > 0 && n_slots > 0, kBadArg, "fused_ffn: empty operand");
+  COMOE_REQUIRE(ldo % 2 == 0 && ldo >= d && (reinterpret_cast<uintptr_t>(out) & 3) == 0,
+                kUnsupportedShape, "fused_ffn: out rows must be 4-byte aligned (ldo even)");
+  COMOE_REQUIRE(slot_stride >= 2L * d * d_ff, kBadArg, "fused_ffn: slot smaller than the expert");
+  COMOE_REQUIRE((row_token == nullptr) == (row_prob == nullptr), kBadArg,
+                "fused_ffn: row_token and row_prob go together");
+  CUtensorMap twi, two, tx;
+  const int kbox = fused_boxes();
+  int rc = make_tmap_bf16_kblk(&twi, pool, n_slots, d_ff, d, slot_stride, 128, kbox);
+  if (rc) return rc;
+  const void* wo = static_cast<const __nv_bfloat16*>(pool) + static_cast<long>(d_ff) * d;
+  rc = make_tmap_bf16_kblk(&two, wo, n_slots, d, d_ff, slot_stride, 128, kbox);
+  if (rc) return rc;
+  rc = make_tmap_bf16_2d(&tx, x, static_cast<uint64_t>(x_rows), d, gather_rows ? 1 : kFTok / 2);
+  if (rc) return rc;
+  FusedFfnParams p{group_rows, group_row_base, group_slot, G, d, d_ff,
+                   reinterpret_cast<__nv_bfloat16*>(out), ldo, row_token, row_prob, gather_rows,
+                   fused_debug()};
+  if (kbox == 1)
+    return gather_rows ? launch_fused<6, 1, true>(twi, two, tx, p, stream)
+                       : launch_fused<6, 1, false>(twi, two, tx, p, stream);
+  return gather_rows ? launch_fused<3, 2, true>(twi, two, tx, p, stream)
+                     : launch_fused<3, 2, false>(twi, two, tx, p, stream);
+}
 
 template <int BN, int kStages, int kMode>
 static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GroupedGemmParams& p,
@@ -253,6 +341,10 @@ int comoe_grouped_ffn(const void* x_perm, long total_rows, int d, int d_ff, int 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   COMOE_REQUIRE(act == COMOE_ACT_RELU || act == COMOE_ACT_SWIGLU, kBadArg, "grouped_ffn: act=%d",
                 act);
+  if (fused_enabled() && fused_supported(d, d_ff, act, G))  // H stays on chip
+    return fused_ffn_impl(x_perm, total_rows, nullptr, d, d_ff, pool, n_slots, slot_stride,
+                          group_rows, group_row_base, group_slot, G, out, ldo, row_token, row_prob,
+                          s);
   COMOE_REQUIRE(h_work != nullptr, kBadArg, "grouped_ffn: null workspace");
   const int n1 = act == COMOE_ACT_SWIGLU ? 2 * d_ff : d_ff;
   int rc = grouped_gemm_impl(x_perm, total_rows, pool, n_slots, slot_stride, 0, n1, d, group_rows,
@@ -264,6 +356,31 @@ int comoe_grouped_ffn(const void* x_perm, long total_rows, int d, int d_ff, int 
   return grouped_gemm_impl(h_work, total_rows, pool, n_slots, slot_stride,
                            static_cast<long>(n1) * d, d, d_ff, group_rows, group_row_base,
                            group_slot, G, mode2, out, ldo, row_token, row_prob, s);
+}
+
+int comoe_fused_ffn_supported(int d, int d_ff, int act, int G) {
+  return comoe::fused_supported(d, d_ff, act, G) ? 1 : 0;
+}
+
+int comoe_fused_ffn_enabled(void) { return comoe::fused_enabled() ? 1 : 0; }
+
+int comoe_fused_ffn(const void* x, long x_rows, const int* gather_rows, int d, int d_ff,
+                    const void* pool, int n_slots, long slot_stride, const int* group_rows,
+                    const int* group_row_base, const int* group_slot, int G, void* out, int ldo,
+                    const int* row_token, const float* row_prob, void* stream) {
+  return comoe::fused_ffn_impl(x, x_rows, gather_rows, d, d_ff, pool, n_slots, slot_stride,
+                               group_rows, group_row_base, group_slot, G, out, ldo, row_token,
+                               row_prob, static_cast<cudaStream_t>(stream));
+}
+
+// dev: per-pair wait cycles of the last fused FFN launched with
+// COMOE_FUSED_DEBUG bit 256 (128 pairs x 16 counters, synchronises)
+int comoe_debug_fused_prof(unsigned long long* out) {
+  using namespace comoe;
+  COMOE_REQUIRE(out, kBadArg, "debug_fused_prof: null pointer");
+  const cudaError_t e = cudaMemcpyFromSymbol(out, g_fprof, sizeof(g_fprof));
+  COMOE_REQUIRE(e == cudaSuccess, kCudaError, "debug_fused_prof: %s", cudaGetErrorString(e));
+  return kOk;
 }
 
 // dev: {clock64, ns} at start and end of CTA 0 of the last 2-SM grouped GEMM

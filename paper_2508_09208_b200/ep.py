@@ -250,12 +250,17 @@ class DeviceOps:
         recv_counts = recv_counts.index_select(0, block).contiguous()
         self.last_recv_counts = recv_counts  # rows this rank computes (bench FLOP count)
         rows = recv_rows.shape[0]
-        h = self._buf(("h", rows), lambda: torch.empty((rows, L.d_ff), dtype=torch.bfloat16,
-                                                       device=dev))
         y = y_out if y_out is not None else self._buf(("y", rows),
                                                        lambda: torch.empty_like(recv_rows))
-        n1 = 2 * L.d_ff if L.act == "swiglu" else L.d_ff
         st = stage if stage is not None else (lambda name: _NoStage())
+        if kernels.fused_ffn_enabled() and kernels.fused_ffn_supported(
+                L.d, L.d_ff, kernels.ACT_RELU if L.act == "relu" else kernels.ACT_SWIGLU, G):
+            with st("ffn"):  # K3F: one launch, H on chip
+                kernels.fused_ffn(recv_rows, L.pool.data, L.d_ff, recv_counts, base, slot, y)
+            return y
+        h = self._buf(("h", rows), lambda: torch.empty((rows, L.d_ff), dtype=torch.bfloat16,
+                                                       device=dev))
+        n1 = 2 * L.d_ff if L.act == "swiglu" else L.d_ff
         with st("ffn1"):
             kernels.grouped_gemm(recv_rows, L.pool.data, 0, n1, recv_counts, base, slot,
                                  kernels.EPI_SWIGLU if L.act == "swiglu" else kernels.EPI_RELU, h)

@@ -306,6 +306,40 @@ def grouped_ffn(x_perm, pool, d_ff, act, group_rows, group_row_base, group_slot,
     return out
 
 
+def fused_ffn_supported(d: int, d_ff: int, act: int, n_groups: int) -> bool:
+    """Whether comoe_fused_ffn takes this shape."""
+    return bool(_lib.load().comoe_fused_ffn_supported(int(d), int(d_ff), int(act), int(n_groups)))
+
+
+def fused_ffn_enabled() -> bool:
+    """The layer forward uses the fused FFN only when opted in
+    (COMOE_FUSED_FFN=1): it measured slower than the two-launch FFN."""
+    return bool(_lib.load().comoe_fused_ffn_enabled())
+
+
+def fused_ffn(x, pool, d_ff, group_rows, group_row_base, group_slot, out, gather_rows=None,
+              row_token=None, row_prob=None):
+    """K3F: relu(X Wi^T) Wo^T per group in one launch, H on chip. `x` is the
+    permuted copy, or (with `gather_rows` = the permute's row_token) the
+    unpermuted tokens, gathered by TMA."""
+    _need(x, "x", torch.bfloat16, 2)
+    _need(pool, "pool", torch.bfloat16, 2)
+    _need(out, "out", torch.bfloat16, 2)
+    for name, t in (("group_rows", group_rows), ("group_row_base", group_row_base),
+                    ("group_slot", group_slot)):
+        _need(t, name, torch.int32, 1)
+    if gather_rows is not None:
+        _need(gather_rows, "gather_rows", torch.int32, 1)
+    rows, d = x.shape
+    if pool.shape[1] < expert_numel(d, d_ff, ACT_RELU):
+        raise ValueError("pool slot too small for the expert shape")
+    _lib.call("comoe_fused_ffn", _ptr(x), rows, _ptr(gather_rows), d, int(d_ff), _ptr(pool),
+              pool.shape[0], pool.shape[1], _ptr(group_rows), _ptr(group_row_base),
+              _ptr(group_slot), group_rows.numel(), _ptr(out), out.shape[1], _ptr(row_token),
+              _ptr(row_prob), _stream())
+    return out
+
+
 def grouped_gemm(a, pool, b_offset, N, group_rows, group_row_base, group_slot, epi_mode, out,
                  row_token=None, row_prob=None, a_gather=None):
     _need(a, "a", torch.bfloat16, 2)

@@ -36,6 +36,12 @@ def _gather_enabled(act: str) -> bool:
         os.environ.get("COMOE_GATHER", "0") == "1"
 
 
+def _fused_gather() -> bool:
+    """The fused FFN reads token rows straight from x with TMA gather4 (no
+    permuted copy; default). COMOE_FUSED_GATHER=0 reads the permuted copy."""
+    return os.environ.get("COMOE_FUSED_GATHER", "1") != "0"
+
+
 class _NoTimer:
     def __enter__(self):
         return self
@@ -115,6 +121,12 @@ class MoELayer:
     def capacity(self, T: int) -> int:
         return kernels.capacity_for(T, self.G, self.top_k, self.capacity_factor)
 
+    @property
+    def fused(self) -> bool:
+        """Whether the forward runs the fused FFN (K3F: one launch, H on chip)."""
+        return kernels.fused_ffn_enabled() and \
+            kernels.fused_ffn_supported(self.d, self.d_ff, ACTS[self.act], self.G)
+
     def _workspace(self, T: int):
         ws = self._ws.get(T)
         if ws is not None:
@@ -123,8 +135,10 @@ class MoELayer:
         C = self.capacity(T)
         rows = max(1, min(T * self.top_k, self.G * C))
         k, nt = self.top_k, kernels.gate_num_tiles(T)
+        fused = self.fused
+        gather = fused and _fused_gather()
         ws = dict(
-            C=C, rows=rows,
+            C=C, rows=rows, fused=fused, gather=gather,
             gate=kernels.GateOutput(
                 torch.empty((T, k), dtype=torch.int32, device=dev),
                 torch.empty((T, k), dtype=torch.int32, device=dev),
@@ -134,11 +148,12 @@ class MoELayer:
             scan=kernels.ScanOutput(torch.empty((k, nt, self.G), dtype=torch.int32, device=dev),
                                     *(torch.empty(self.G, dtype=torch.int32, device=dev)
                                       for _ in range(3))),
-            perm=kernels.PermuteOutput(torch.empty((rows, self.d), dtype=torch.bfloat16, device=dev),
+            perm=kernels.PermuteOutput(torch.empty((1 if gather else rows, self.d),
+                                                   dtype=torch.bfloat16, device=dev),
                                        torch.empty(rows, dtype=torch.int32, device=dev),
                                        torch.empty(rows, dtype=torch.float32, device=dev),
                                        torch.empty((T, k), dtype=torch.int32, device=dev)),
-            h=torch.empty((rows, self.d_ff), dtype=torch.bfloat16, device=dev),
+            h=None if fused else torch.empty((rows, self.d_ff), dtype=torch.bfloat16, device=dev),
             y_perm=torch.empty((rows, self.d), dtype=torch.bfloat16, device=dev) if k > 1 else None,
         )
         self._ws[T] = ws
@@ -186,11 +201,27 @@ class MoELayer:
         with stage("route"):
             r = self.route(x, want_logits, routing=routing)
         k1 = self.top_k == 1
+        dst = out if k1 else ws["y_perm"]
+        if ws["fused"]:
+            gather = ws["gather"]
+            with stage("permute"):  # (index tables only when the FFN gathers the rows)
+                kernels.permute(x, r.gate, r.scan, r.capacity, r.rows,
+                                y_zero=out if k1 else None, out=r.perm, copy_rows=not gather)
+            with stage("ffn"):
+                kernels.fused_ffn(x if gather else r.perm.x_perm, self.pool.data, self.d_ff,
+                                  r.scan.group_kept, r.scan.group_base, self.group_slot, dst,
+                                  gather_rows=r.perm.row_token if gather else None,
+                                  row_token=r.perm.row_token if k1 else None,
+                                  row_prob=r.perm.row_prob if k1 else None)
+            if not k1:
+                with stage("combine"):
+                    kernels.combine(ws["y_perm"], r.perm.token_pos, r.gate.gate_prob, out=out)
+            self.last = r
+            return out
         gather = _gather_enabled(self.act)
         with stage("permute"):
             kernels.permute(x, r.gate, r.scan, r.capacity, r.rows, y_zero=out if k1 else None,
                             out=r.perm, copy_rows=not gather)
-        dst = out if k1 else ws["y_perm"]
         n1 = 2 * self.d_ff if self.act == "swiglu" else self.d_ff
         with stage("ffn1"):
             kernels.grouped_gemm(x if gather else r.perm.x_perm, self.pool.data, 0, n1,
@@ -213,8 +244,9 @@ class MoELayer:
 
     @property
     def kernels_per_forward(self) -> int:
-        """Device kernels one forward launches (gate, scan, permute, 2x GEMM [, combine])."""
-        return 5 + (0 if self.top_k == 1 else 1)
+        """Device kernels one forward launches: gate, scan, permute, FFN (one
+        fused launch or two GEMMs) [, combine]."""
+        return (4 if self.fused else 5) + (0 if self.top_k == 1 else 1)
 
     def capture(self, x: torch.Tensor, out: torch.Tensor = None) -> "CapturedForward":
         """Record one forward over the static buffers `x` (and `out`) as a

@@ -27,7 +27,12 @@ def test_library_exports_all_declared_symbols():
     for name in _declared():
         assert hasattr(lib, name), name
     assert set(_declared()) == set(_lib.EXPORTED)
-    assert lib.comoe_version() == 1
+    assert lib.comoe_version() == _lib.ABI_VERSION == 2
+    # fused FFN shape gate (host-side; no device needed)
+    assert lib.comoe_fused_ffn_supported(768, 3072, 0, 128) == 1
+    assert lib.comoe_fused_ffn_supported(1024, 3072, 0, 128) == 0   # Y + H exceed TMEM
+    assert lib.comoe_fused_ffn_supported(4096, 14336, 1, 8) == 0    # SwiGLU: two launches
+    assert lib.comoe_fused_ffn_enabled() in (0, 1)                  # opt-in: COMOE_FUSED_FFN=1
     assert lib.comoe_gate_padded_experts(8) == 16
     assert lib.comoe_gate_padded_experts(128) == 128
     assert lib.comoe_gate_padded_experts(129) == -1
