@@ -47,6 +47,21 @@ def bf16_round(a) -> np.ndarray:
     return out
 
 
+def det_uniform(shape, seed: int, scale: float) -> np.ndarray:
+    """Deterministic test inputs: a counter-based splitmix64 stream mapped to
+    uniform(-1, 1) * scale * sqrt(3) (unit variance before `scale`), float32.
+    Bit-identical on every numpy version (no library RNG), so golden
+    fixtures store seeds instead of tensors (oracle/gen_layer_golden.py)."""
+    n = int(np.prod(shape))
+    with np.errstate(over="ignore"):
+        z = np.arange(n, dtype=np.uint64) + np.uint64(seed) * np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    u = (z >> np.uint64(11)).astype(np.float64) * (1.0 / 2 ** 53)
+    return ((2.0 * u - 1.0) * math.sqrt(3.0) * scale).astype(np.float32).reshape(shape)
+
+
 def gate_logits(x, wg) -> np.ndarray:
     """fp32 router logits of bf16-valued x[T,d] and fp32 Wg[d,E]."""
     return (np.asarray(x, np.float64) @ np.asarray(wg, np.float64)).astype(np.float32)
@@ -248,13 +263,16 @@ def dispatch_fast(group, n_groups: int, cap: int):
 
 
 def layer_forward_fast(x, wg, w_in, w_out, top_k=1, norm_topk=False, capacity_factor=1.25,
-                       slot_map=None, act="relu", dtype=np.float32):
+                       slot_map=None, act="relu", dtype=np.float32, logits=None, round_h=False):
     """CPU forward with NumPy BLAS: x [T,d], wg [d,E], w_in [G,N1,d],
-    w_out [G,d,d_ff] (already `dtype`). Returns y [T,d] (dtype)."""
+    w_out [G,d,d_ff] (arrays or per-group lists, already `dtype`). Returns
+    y [T,d] (dtype). `logits` feeds given fp32 logits (parity "given
+    identical logits"); `round_h` rounds H to bf16 like the device."""
     x = np.asarray(x, dtype)
-    logits = (x @ np.asarray(wg, dtype)).astype(np.float32)
+    if logits is None:
+        logits = (x @ np.asarray(wg, dtype)).astype(np.float32)
     idx, group, prob = topk_route(logits, top_k, norm_topk, slot_map)
-    G = w_in.shape[0]
+    G = len(w_in)
     cap = capacity(x.shape[0], G, top_k, capacity_factor)
     disp = dispatch_fast(group, G, cap)
     y = np.zeros_like(x)
@@ -271,6 +289,8 @@ def layer_forward_fast(x, wg, w_in, w_out, top_k=1, norm_topk=False, capacity_fa
             n1 = a.shape[1]
             b = a.reshape(n, n1 // (2 * SWIGLU_BLOCK), 2, SWIGLU_BLOCK)
             h = (b[:, :, 0] / (1 + np.exp(-b[:, :, 0])) * b[:, :, 1]).reshape(n, n1 // 2)
+        if round_h:
+            h = bf16_round(h.astype(np.float32)).astype(dtype)
         rows[lo:lo + n] = h @ w_out[g].T
     for j in range(top_k):
         p = disp["pos"][:, j]

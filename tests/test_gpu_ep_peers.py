@@ -89,8 +89,8 @@ def test_peer_transport_matches_alltoall_schedule(world, T, E, cf):
     wo = np.stack([O.split_expert(w[e].float().numpy(), d, d_ff, "relu")[1] for e in range(E)])
     for r in range(world):
         y_ref, info = O.layer_forward_fast(xs[r].float().cpu().numpy(), wg.numpy(), wi, wo, 1,
-                                           False, cf, dtype=np.float64)
-        assert O.normwise_error(outs[r].float().cpu().numpy(), y_ref) < 1e-2
+                                           False, cf, dtype=np.float64, round_h=True)
+        assert O.normwise_error(outs[r].float().cpu().numpy(), y_ref) < 5e-3  # bf16 bar
 
 
 def test_peer_barrier_concurrent_ranks_and_timeout():

@@ -180,8 +180,14 @@ def test_forward_is_deterministic():
     assert torch.equal(r1, layer.last.perm.row_token)
 
 
-def test_full_size_properties_sb128():
-    """C2 shape (T=65536, E=128, cf=1.25): size-independent properties."""
+def test_full_size_c2_sb128():
+    """C2 shape (T=65536, E=128, cf=1.25), compared whole:
+    * logits within 2e-5 of the fp64 oracle for every token;
+    * expert choice, per-group counts / kept / bases, every token's row and
+      the full row -> token permutation bit-exact against the oracle's
+      vectorised dispatch on the device logits;
+    * the whole output within the bf16 bar of the oracle forward (fp32 BLAS,
+      H rounded to bf16 like the device), dropped tokens exactly 0."""
     T, d, d_ff, E = 65536, 768, 3072, 128
     from paper_2508_09208_b200 import ExpertPool, MoELayer
     torch.manual_seed(0)
@@ -194,29 +200,30 @@ def test_full_size_properties_sb128():
     torch.cuda.synchronize()
     r = layer.last
     assert r.capacity == 640
-    count = r.scan.group_count.cpu().numpy()
-    kept = r.scan.group_kept.cpu().numpy()
-    assert count.sum() == T
-    np.testing.assert_array_equal(kept, np.minimum(count, 640))
-    pos = r.perm.token_pos.cpu().numpy()[:, 0]
-    assert (pos >= 0).sum() == kept.sum()
-    # permutation is a bijection onto [0, kept.sum())
-    assert np.array_equal(np.sort(pos[pos >= 0]), np.arange(kept.sum()))
-    # routing equals the oracle's on the device logits (vectorised check)
+    xs, wgs = _np(x), _np(wg)
     logits = r.gate.logits.cpu().numpy()
+    ref_logits = O.gate_logits(xs, wgs).astype(np.float64)
+    assert np.max(np.abs(logits.astype(np.float64) - ref_logits)) < LOGIT_ABS_TOL
     idx, grp, prob = O.topk_route(logits, 1, False)
     np.testing.assert_array_equal(r.gate.expert_idx.cpu().numpy(), idx)
-    # spot-check 256 tokens of the output against the oracle expert FFN
-    rng = np.random.default_rng(0)
-    toks = rng.choice(np.nonzero(pos >= 0)[0], 256, replace=False)
-    xs = x[torch.as_tensor(toks).cuda()].float().cpu().numpy()
-    ref = np.zeros((len(toks), d))
-    for i, t in enumerate(toks):
-        e = int(idx[t, 0])
-        w_in, w_out = O.split_expert(pool.view(e).float().cpu().numpy(), d, d_ff, "relu")
-        ref[i] = prob[t, 0] * O.expert_ffn(xs[i:i + 1], w_in, w_out, "relu")[0]
-    assert O.normwise_error(y[torch.as_tensor(toks).cuda()].float().cpu().numpy(), ref) < NORMWISE_TOL
-    assert torch.all(y[torch.as_tensor(np.nonzero(pos < 0)[0]).cuda()] == 0)
+    assert np.max(np.abs(r.gate.gate_prob.cpu().numpy() - prob)) < PROB_TOL
+    disp = O.dispatch_fast(grp, E, 640)
+    np.testing.assert_array_equal(r.scan.group_count.cpu().numpy(), disp["count"])
+    np.testing.assert_array_equal(r.scan.group_kept.cpu().numpy(), disp["kept"])
+    np.testing.assert_array_equal(r.scan.group_base.cpu().numpy(), disp["base"])
+    np.testing.assert_array_equal(r.perm.token_pos.cpu().numpy(), disp["pos"])
+    rows = int(disp["kept"].sum())
+    np.testing.assert_array_equal(r.perm.row_token[:rows].cpu().numpy(), disp["row_token"])
+    w = pool.data[:, :2 * d * d_ff].float().cpu().numpy()
+    w_in = w[:, :d_ff * d].reshape(E, d_ff, d)
+    w_out = w[:, d_ff * d:].reshape(E, d, d_ff)
+    del w
+    ref, _ = O.layer_forward_fast(xs, wgs, w_in, w_out, 1, False, 1.25, logits=logits,
+                                  round_h=True)
+    got = _np(y)
+    assert O.normwise_error(got, ref) < NORMWISE_TOL
+    dropped = disp["pos"][:, 0] < 0
+    assert dropped.any() and (got[dropped] == 0).all()
 
 
 def test_replayed_trace_routing_matches_oracle():

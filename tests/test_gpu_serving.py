@@ -62,9 +62,9 @@ def test_expert_parallel_world1_matches_oracle():
     wi = np.stack([O.split_expert(w[e].float().numpy(), d, d_ff, "relu")[0] for e in range(E)])
     wo = np.stack([O.split_expert(w[e].float().numpy(), d, d_ff, "relu")[1] for e in range(E)])
     ref, info = O.layer_forward_fast(x.float().numpy(), wg.cpu().numpy(), wi, wo, 1, False, 1.0,
-                                     dtype=np.float64)
+                                     dtype=np.float64, round_h=True)
     assert (info["pos"] < 0).sum() > 0
-    assert O.normwise_error(y.float().cpu().numpy(), ref) < 1e-2
+    assert O.normwise_error(y.float().cpu().numpy(), ref) < 5e-3  # the bf16 bar
     dist.destroy_process_group()
 
 
