@@ -17,6 +17,9 @@ Fixtures
   policy_cases.json    cache-policy decisions: prefetch_threshold, eviction
                        scores, evict victims / infeasible, decide_prefetch,
                        plan_initial_placement, correct_misprediction
+  priority_cases.json  offload_priority values and error cases
+  traces.json          generate_routing traces (+ the reference's
+                       collect_stats of each) and a trained predictor
 """
 
 from __future__ import annotations
@@ -223,6 +226,9 @@ def traces_and_predictor(moe, off):
                    experts=[[list(tok.layer_experts[l]) for l in spec.moe_layer_indices] for tok in tr.tokens],
                    emb_sum=float(sum(float(t.embedding.sum()) for t in tr.tokens)),
                    ctx_sum=float(sum(float(t.context.sum()) for t in tr.tokens)))
+        st = moe.collect_stats(tr)  # the reference's ActivationStats of this trace
+        rec["collect_stats"] = dict(counts={str(l): st.counts[l].tolist() for l in st.counts},
+                                    totals={str(l): int(st.totals[l]) for l in st.totals})
         if i == 0:
             big = moe.generate_routing(g, spec, 300)
             mlp, metrics = off.train_predictor(big, hidden_dim=8, lr=0.05, epochs=2, seed=5)
@@ -233,8 +239,32 @@ def traces_and_predictor(moe, off):
     return out
 
 
+def priority_cases(off, n_cases=40):
+    """offload_priority (offload.py:430-438) on seeded inputs, including the
+    simulator's uniform-size use (normalizer = size / estimate,
+    simulator.py:423-431) and the error cases."""
+    rng = np.random.default_rng(20261017)
+    cases = []
+    for i in range(n_cases):
+        f = float(rng.random()) if i % 5 else 0.0
+        size = float(rng.choice([9437184.0, 352321536.0, rng.random() * 1e9 + 1]))
+        est = float(rng.random() * 1e-2 + 1e-6)
+        gamma = float(rng.choice([0.0, 1.0, rng.random()]))
+        norm = size / est if i % 2 else float(rng.random() * 1e11 + 1.0)
+        cases.append(dict(args=[f, size, est, gamma, norm],
+                          value=off.offload_priority(f, size, est, gamma, norm)))
+    for bad in ([0.5, 1.0, 0.0, 0.5, 1.0], [0.5, 1.0, 1.0, 0.5, 0.0]):
+        try:
+            off.offload_priority(*bad)
+            raise AssertionError("expected ValueError")
+        except ValueError as e:
+            cases.append(dict(args=bad, error=str(e)))
+    return cases
+
+
 def main():
     moe, agg, off = _ref()
+    (OUT / "priority_cases.json").write_text(json.dumps(priority_cases(off), indent=1))
     (OUT / "traces.json").write_text(json.dumps(traces_and_predictor(moe, off)))
     OUT.mkdir(parents=True, exist_ok=True)
     (OUT / "fusion_cases.json").write_text(json.dumps(fusion_cases(moe, agg)))

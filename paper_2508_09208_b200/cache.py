@@ -205,7 +205,7 @@ class ExpertCache:
                     self.state.record_access(dec.expert, self.tick)
                     self.state.pinned.add(dec.expert)
                     out[eid] = self.slot_of[dec.expert]
-                    self.stats.events.append(("substitute", eid))
+                    self.stats.events.append(("substitute", eid, dec.expert))
                     continue
             if self._room_in_workspace():
                 tier = WORKSPACE
@@ -296,9 +296,12 @@ def activate_variant(variant, layer: int, stats, host_experts: torch.Tensor, bud
     freqs = {(layer, i): freqs_all[(layer, p)] for i, p in enumerate(principals)}
     numel = host_experts.shape[1]
     ebytes = float(numel * host_experts.element_size())
+    # _resident_budget (simulator.py:275-286) never keeps more than the
+    # variant itself resident; the batched runtime adds its workspace slots
+    # (one wave of demanded experts) on top, and no more
     ws_cap = min(workspace_slots * top_k * ebytes, budget_bytes)
-    n_slots = int(budget_bytes // ebytes)
     ws_slots = max(1, int(ws_cap // ebytes))
+    n_slots = min(int(budget_bytes // ebytes), len(principals) + ws_slots)
     if n_slots <= ws_slots:
         raise InfeasibleError(f"budget {budget_bytes:.3e} B holds {n_slots} experts; need more than "
                               f"the {ws_slots}-expert workspace")
@@ -366,8 +369,10 @@ class CachedMoELayer:
         order = [int(g) for g in np.argsort(-kept, kind="stable") if kept[g] > 0]
         hits = [g for g in order if c.state.resident((c.layer, g))]
         misses = [g for g in order if not c.state.resident((c.layer, g))]
-        seq = hits + misses
-        waves = [seq[i:i + self.wave_slots] for i in range(0, len(seq), self.wave_slots)]
+        # every hit is already resident: one wave serves them all (no copies,
+        # no slots needed); only misses are bounded by the free slots
+        waves = ([hits] if hits else []) + \
+            [misses[i:i + self.wave_slots] for i in range(0, len(misses), self.wave_slots)]
         n1 = 2 * L.d_ff if L.act == "swiglu" else L.d_ff
         dst = out if k1 else ws["y_perm"]
         epi1 = kernels.EPI_SWIGLU if L.act == "swiglu" else kernels.EPI_RELU

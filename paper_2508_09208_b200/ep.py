@@ -330,11 +330,21 @@ class EPMoELayer:
                                      self.local.wg.device, group=self.group)
         return self.peers
 
+    # peer transport: a barrier that times out sets a sticky error flag
+    # instead of hanging; forward() reads it (one host sync) every
+    # `err_check_every` calls outside CUDA-graph capture and raises, so a
+    # dead or late peer cannot leave partially written outputs unnoticed
+    err_check_every = 8
+
     def forward(self, x, out=None, timer=None):
         C = self.capacity(x.shape[0])
         if self.transport == "peer":
-            y = ep_forward_peers(x, self.ops, self.peer_buffers(x.shape[0]), self.E, C,
-                                 stage=timer)
+            bufs = self.peer_buffers(x.shape[0])
+            y = ep_forward_peers(x, self.ops, bufs, self.E, C, stage=timer)
+            self._calls = getattr(self, "_calls", 0) + 1
+            if self._calls % self.err_check_every == 0 and \
+                    not torch.cuda.is_current_stream_capturing():
+                bufs.check()
         else:
             y = ep_forward(x, self.ops, self.world, self.E, C, group=self.group, stage=timer)
         if out is not None:

@@ -31,10 +31,21 @@ class ExpertPool:
     def slot_bytes(self) -> int:
         return self.numel * self.data.element_size()
 
-    def alloc(self) -> int:
+    def alloc(self, exclude=()) -> int:
+        """A free slot, never one of `exclude` (e.g. slots holding experts
+        that were written through `data` without alloc(): they are reserved
+        on the way, so later allocations skip them too)."""
+        ex = set(exclude)
+        for s in [s for s in self._free if s in ex]:
+            self._free.remove(s)
         if not self._free:
             raise RuntimeError("expert pool is full")
         return self._free.pop()
+
+    def reserve(self, slot: int) -> None:
+        """Mark a slot filled through `data` as in use."""
+        if slot in self._free:
+            self._free.remove(slot)
 
     def release(self, slot: int) -> None:
         if not 0 <= slot < self.n_slots or slot in self._free:

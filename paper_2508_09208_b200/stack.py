@@ -25,9 +25,25 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import numpy as np
 import torch
 
 from .offload import OffloadPolicy, prefetch_threshold
+
+
+def fold_demand(demand, slot_map, n_groups: int) -> np.ndarray:
+    """Per-original-expert demand probabilities of the next layer -> its
+    cache's group space (a fused variant's experts are (layer, group)):
+    P(group g demanded) = 1 - prod_{e in g} (1 - p_e). The reference folds
+    its per-token predictor output the same way before decide_prefetch,
+    with a sum (np.add.at(merged, map_arrays[nxt], raw), simulator.py:587-588);
+    for the batch demand probabilities here the complement product is the
+    consistent fold (it stays a probability)."""
+    demand = np.clip(np.asarray(demand, np.float64), 0.0, 1.0)
+    lut = np.asarray(slot_map, np.int64)
+    miss = np.ones(n_groups)
+    np.multiply.at(miss, lut, 1.0 - demand[:len(lut)])
+    return 1.0 - miss
 
 
 @dataclass
@@ -59,7 +75,8 @@ class CachedMoEStack:
                 def hook(r, sl=sl, nxt=nxt):
                     _, demand = self.predictor.predict_slots(r.gate.expert_idx, emb, ctx,
                                                              want_demand=True, demand_mode="any")
-                    demand = demand.cpu().numpy()
+                    L = nxt.layer.layer
+                    demand = fold_demand(demand.cpu().numpy(), L.slot_map.cpu().numpy(), L.G)
                     chosen = nxt.layer.cache.prefetch(demand, self.theta)
                     self.prefetch_log.append((sl.index, nxt.index, chosen))
             y = sl.layer.forward(h, after_route=hook,

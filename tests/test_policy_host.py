@@ -154,3 +154,39 @@ def test_resident_budget_modes_match_simulator_rules():
     v = A.ModelVariant("x", {}, {}, {}, 0.0, 1.0, expert_bytes=40.0)
     req = required_bytes_fn("fraction_of_variant", 0.5, 100.0, m_other=3.0, workspace_bytes=2.0)
     assert req(v) == 25.0
+
+
+def test_fold_demand_into_group_space():
+    """stack.fold_demand: P(group demanded) = 1 - prod over its members."""
+    from paper_2508_09208_b200.stack import fold_demand
+    p = np.array([0.5, 0.2, 0.0, 1.0, 0.3])
+    lut = [0, 0, 1, 2, 1]
+    out = fold_demand(p, lut, 3)
+    np.testing.assert_allclose(out, [1 - 0.5 * 0.8, 1 - 1.0 * 0.7, 1.0])
+    np.testing.assert_allclose(fold_demand(p, range(5), 5), p)  # identity variant: unchanged
+
+
+def test_pool_alloc_skips_excluded_slots_and_reserves_them():
+    from paper_2508_09208_b200.pool import ExpertPool
+    pool = ExpertPool(6, 64, device="cpu")
+    a = pool.alloc(exclude={0, 1})
+    assert a not in (0, 1)
+    assert pool.free_slots() == 3                    # 0 and 1 reserved, a taken
+    assert all(pool.alloc() not in (0, 1, a) for _ in range(3))
+    pool.reserve(0)                                  # already reserved: no-op
+    with pytest.raises(RuntimeError):
+        pool.alloc()
+
+
+def test_offload_priority_matches_reference():
+    """a19: offload_priority (offload.py:430-438) on reference-generated
+    cases (oracle/gen_golden.py -> priority_cases.json), bit for bit."""
+    from paper_2508_09208_b200.offload import offload_priority
+    cases = json.loads((GOLDEN / "priority_cases.json").read_text())
+    assert len(cases) > 40
+    for c in cases:
+        if "error" in c:
+            with pytest.raises(ValueError, match=c["error"]):
+                offload_priority(*c["args"])
+        else:
+            assert offload_priority(*c["args"]) == c["value"]

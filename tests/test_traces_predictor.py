@@ -72,3 +72,15 @@ def test_presets():
     assert abs(b - 9_635_416.67) < 1
     with pytest.raises(Exception):
         presets.preset_geometry("sb7")
+
+
+@pytest.mark.parametrize("c", CASES, ids=lambda c: f"E{c['E']}k{c['K']}")
+def test_collect_stats_matches_reference(c):
+    """a3: collect_stats (moe.py:250-262) of the reference-identical trace
+    equals the reference's own ActivationStats (traces.json)."""
+    tr = generate_routing(_gspec(c), _spec(c), c["n"])
+    st = collect_stats(tr)
+    ref = c["collect_stats"]
+    for l in tr.moe_layer_indices:
+        np.testing.assert_array_equal(st.counts[l], np.asarray(ref["counts"][str(l)]))
+        assert st.totals[l] == ref["totals"][str(l)]
