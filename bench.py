@@ -34,7 +34,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "MoE-layer tokens/sec (Switch-Base-128 shape) + % roofline at 1/2/4/8 B200"
 UNIT = "tokens/s"
 T_PER_GPU, D, D_FF, E, TOP_K, CF = 65536, 768, 3072, 128, 1, 1.25
-CPU_SAMPLE_TOKENS = 16384
+CPU_SAMPLE_TOKENS = T_PER_GPU  # the CPU port runs the full C2 batch (C = 640), ~1 s per forward
 L2_BYTES = 126 * 2 ** 20
 
 
@@ -137,6 +137,136 @@ def cpu_layer_sample(tokens: int, seed: int = 0, reps: int = 3):
     return tokens / best, best, threads
 
 
+def _reference_package():
+    """The unmodified reference package installed offline into baseline/_ref
+    (DESIGN.md §6), or None when the lease does not carry it."""
+    ref = ROOT / "baseline" / "_ref"
+    if (ref / "comoe").is_dir() and str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    try:
+        from comoe import aggregation, moe  # noqa: F401
+        return aggregation, moe
+    except ImportError:
+        return None
+
+
+def fusion_cpu_baseline(dev=None):
+    """the reference's own merge_group / fuse_model timed on
+    this host (from baseline/_ref; else oracle/merge.py, bit-exact to it),
+    fp64 as the reference computes, beside the device K5 merge / fuse_model
+    on the same experts (bf16). Shapes: C1 (Switch-Base-8, D = 4,718,592, a
+    2-member group; fuse_model 8 -> 4 with the default 8x8 calibration), C2
+    (one 3-member group of Switch-Base-128), C5 (Mixtral, D = 176,160,768, a
+    2-member group)."""
+    import numpy as np
+    out = {}
+    refpkg = _reference_package()
+    kind = "reference" if refpkg else "port"
+    out["kind"] = kind
+    out["source"] = "baseline/_ref comoe (unmodified reference)" if refpkg else \
+        "oracle/merge.py (bit-exact restatement)"
+    rng = np.random.default_rng(0)
+
+    def best(fn, reps):
+        b = float("inf")
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            b = min(b, time.perf_counter() - t0)
+        return b
+
+    def cpu_merge(vecs, freqs):
+        if refpkg:
+            A, M = refpkg
+            E_ = len(vecs)
+            ex = {s: M.Expert(layer=1, slot=s, params=v, size=1.0) for s, v in enumerate(vecs)}
+            st = M.ActivationStats(counts={1: np.asarray(freqs, float) * 100},
+                                   totals={1: 100}, experts_per_layer=E_)
+            grp = A.ExpertGroup(principal_slot=0, member_slots=tuple(range(1, E_)))
+            return lambda: A.merge_group(grp, ex, st, 1)
+        from oracle import merge as OM
+        return lambda: OM.merge_params(vecs, freqs)
+
+    for name, D_, n in (("c1_merge_group", 2 * 768 * 3072, 2), ("c2_merge_group", 2 * 768 * 3072, 3),
+                        ("c5_merge_group", 3 * 4096 * 14336, 2)):
+        vecs = [rng.standard_normal(D_) * 0.02 for _ in range(n)]
+        freqs = list(rng.random(n) * 0.1 + 0.01)
+        secs = best(cpu_merge(vecs, freqs), 2 if D_ < 10 ** 8 else 1)
+        rec = {"cpu_s": secs, "bytes": (n + 1) * D_ * 8, "cpu_GBps": (n + 1) * D_ * 8 / secs / 1e9}
+        if dev is not None:
+            import torch
+            from paper_2508_09208_b200 import kernels
+            V = torch.as_tensor(np.stack(vecs), device=dev).to(torch.bfloat16)
+            o = torch.empty(D_, dtype=torch.bfloat16, device=dev)
+            plan = kernels.MergePlan([[V[i] for i in range(n)]], [freqs], [float(sum(freqs))],
+                                     [o], torch.bfloat16)  # group table uploaded once
+            run = plan.run
+            run()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(10):
+                run()
+            b.record()
+            torch.cuda.synchronize()
+            rec["gpu_ms_bf16"] = a.elapsed_time(b) / 10
+            rec["gpu_GBps_bf16"] = (n + 1) * D_ * 2 / (rec["gpu_ms_bf16"] * 1e-3) / 1e9
+            del V, o, plan
+        out[name] = rec
+        del vecs
+    # fuse_model at C1: 8 experts, fixed retention 0.5, alpha 0.5, make_calibration defaults
+    D1, E1 = 2 * 768 * 3072, 8
+    P = rng.standard_normal((E1, D1)) * 0.02
+    counts = rng.integers(1, 500, size=E1).astype(float)
+    if refpkg:
+        A, M = refpkg
+        spec = M.MoeModelSpec(total_layers=1, encoder_moe_layers=(1,), decoder_moe_layers=(),
+                              experts_per_layer=E1, expert_size_bytes=D1 * 2.0, top_k=1,
+                              expert_param_dim=D1)
+        model = M.MoeModel(spec, {(1, s): M.Expert(1, s, P[s], D1 * 2.0) for s in range(E1)})
+        st = M.ActivationStats(counts={1: counts}, totals={1: int(counts.sum())},
+                               experts_per_layer=E1)
+        calib = M.make_calibration(D1)
+        t0 = time.perf_counter()
+        A.fuse_model(model, st, A.FusionConfig(mode="fixed", r=0.5), 0.5, calib)
+        out["c1_fuse_model"] = {"cpu_s": time.perf_counter() - t0}
+    if dev is not None and "c1_fuse_model" in out:
+        import torch
+        from paper_2508_09208_b200 import ExpertPool
+        from paper_2508_09208_b200 import aggregation as PA
+        from paper_2508_09208_b200 import moe as PM
+        pool = ExpertPool(E1 + 8, D1, device=dev)
+        pool.data[:E1, :D1].copy_(torch.as_tensor(P, device=dev).to(torch.bfloat16))
+        for _ in range(E1):
+            pool.alloc()
+        pspec = PM.MoeModelSpec(1, (1,), (), E1, D1 * 2.0, 1, D1)
+        pmodel = PM.MoeModel(pspec, {(1, s): PM.Expert(1, s, pool.view(s), D1 * 2.0)
+                                     for s in range(E1)})
+        pst = PM.ActivationStats(counts={1: counts}, totals={1: int(counts.sum())},
+                                 experts_per_layer=E1)
+        pcal = PM.make_calibration(D1)
+        cfg = PA.FusionConfig(mode="fixed", r=0.5)
+        PA.fuse_model(pmodel, pst, cfg, 0.5, pcal, pool=pool).release_slots(pool)  # warm
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        v = PA.fuse_model(pmodel, pst, cfg, 0.5, pcal, pool=pool)
+        torch.cuda.synchronize()
+        out["c1_fuse_model"]["gpu_ms_bf16"] = (time.perf_counter() - t0) * 1e3
+        v.release_slots(pool)
+        del pool
+    return out
+
+
+def _cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -146,7 +276,7 @@ def run_reference(args):
     from oracle import switch_layer as O
     threads = len(os.sched_getaffinity(0))
     rng = np.random.default_rng(0)
-    tok = 4096  # one bounded sample per step
+    tok = T_PER_GPU  # each step is one full C2 batch (65,536 tokens, C = 640)
     x = O.bf16_round(rng.standard_normal((tok, D), dtype=np.float32))
     wg = (rng.standard_normal((D, E), dtype=np.float32) / math.sqrt(D)).astype(np.float32)
     w_in = O.bf16_round(rng.standard_normal((E, D_FF, D), dtype=np.float32) * 0.02)
@@ -158,8 +288,9 @@ def run_reference(args):
         O.layer_forward_fast(x, wg, w_in, w_out, TOP_K, False, CF)
     dt = time.perf_counter() - t0
     value = tok * args.steps / dt
-    sample = (f"{tok} tokens per step of the C2 layer (E=128, cf 1.25 -> C=40), NumPy fp32 BLAS "
-              f"oracle port of the layer forward, {threads} host threads")
+    sample = (f"{tok} tokens per step: the full C2 batch (E=128, cf 1.25 -> C=640), NumPy fp32 "
+              f"BLAS oracle port of the layer forward (the reference has none), {threads} host "
+              f"threads")
     _emit({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
@@ -195,7 +326,8 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1 or args.force_ep:
-        os.environ.setdefault("NCCL_DEBUG", "WARN")  # stdout carries exactly one JSON line
+        # (NCCL's own log lines go to stderr: _claim_stdout points fd 1 there,
+        # so the driver's NCCL_DEBUG=INFO communicator checks keep working)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29555")
         dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
@@ -361,8 +493,14 @@ def run_ours(args):
         os.environ.setdefault("OPENBLAS_NUM_THREADS", str(len(os.sched_getaffinity(0))))
         v, secs, threads = cpu_layer_sample(CPU_SAMPLE_TOKENS)
         cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"{CPU_SAMPLE_TOKENS} tokens of the C2 layer (cf 1.25 -> C=160), "
-                         f"NumPy fp32 BLAS oracle port, best of 3 ({secs:.2f} s each)"}
+               "sample": f"{CPU_SAMPLE_TOKENS} tokens = the full C2 batch (cf 1.25 -> C=640), "
+                         f"NumPy fp32 BLAS oracle port, best of 3 ({secs:.2f} s each)",
+               "cpu_model": _cpu_model()}
+        try:
+            cpu["fusion"] = fusion_cpu_baseline(dev)
+            cpu["fusion"]["cores"] = threads
+        except Exception as exc:  # the layer baseline stands on its own
+            cpu["fusion"] = {"error": repr(exc)[:200]}
 
     launches = getattr(layer, "kernels_per_forward", 6) * args.steps
     if rank == 0:
