@@ -18,6 +18,9 @@ Fixtures
                        scores, evict victims / infeasible, decide_prefetch,
                        plan_initial_placement, correct_misprediction
   priority_cases.json  offload_priority values and error cases
+  cache_parity.json    the reference runtime's per-token cache decision
+                       stream (hit / fetch / substitute / prefetch /
+                       demote / evict) on a small scenario + its inputs
   traces.json          generate_routing traces (+ the reference's
                        collect_stats of each) and a trained predictor
 """
@@ -262,8 +265,96 @@ def priority_cases(off, n_cases=40):
     return cases
 
 
+PARITY_SCENARIO = {
+    # small geometry on one device: 3 MoE layers x 8 experts, 1 MB experts;
+    # an absolute 13-expert HBM budget (1 workspace + 12 cache slots, the
+    # decoder layer's 8 experts pinned), MLP predictor with a constant
+    # prefetch threshold, substitution on, and a host link fast enough that
+    # every prefetch lands before its next use (no late-prefetch timing).
+    # 192 tokens exercise every decision kind: hit, fetch, substitute,
+    # prefetch, demote, evict
+    "model": {"preset": None, "total_layers": 4, "encoder_moe_layers": [1, 2],
+              "decoder_moe_layers": [3], "experts_per_layer": 8, "top_k": 1,
+              "expert_size_bytes": 1.0e6, "expert_param_dim": 64},
+    "fusion": {"enabled": False},
+    "offload": {"enabled": True, "cache_mode": "absolute", "cache_bytes": 13.0e6,
+                "workspace_slots": 1, "predictor": "mlp", "predictor_hidden": 16,
+                "predictor_epochs": 3, "prefetch": True, "threshold_mode": "constant",
+                "theta_base": 0.1, "substitution": True, "substitution_sim_min": 0.5,
+                "pin_decoder": True},
+    "resources": {"devices": [{"device_id": "parity",
+                               "base": {"gpu_mem_total": 8.0e9, "bw_gpu_cpu": 1.0e15}}]},
+    "workload": {"sequence_length": 64, "sequences": 3,
+                 "routing": {"mode": "generate", "skew": 1.2, "rho": 0.9, "seed": 77,
+                             "structure_seed": 5}},
+}
+
+
+def cache_parity(moe):
+    """The reference runtime's per-token cache loop (simulator.py:684-724,
+    _serve_demand / _predict_and_prefetch / eviction) on PARITY_SCENARIO:
+    its decision event stream plus every input needed to replay the same
+    decisions through the B200 cache (trace, predictor weights, merged
+    frequencies, similarities, offload priorities, initial placement)."""
+    import copy
+    from comoe import scenario as scen
+    from comoe import simulator as sim
+    captured = []
+
+    class _Captured(sim._Run):  # records the run object (no behaviour change)
+        def __init__(self, *a, **k):
+            super().__init__(*a, **k)
+            captured.append(self)
+
+        def _activate_variant(self, variant, tick):
+            super()._activate_variant(variant, tick)
+            self._initial_cache = copy.deepcopy(self.cache)
+
+    orig = sim._Run
+    sim._Run = _Captured
+    try:
+        report = sim.run_inference(copy.deepcopy(PARITY_SCENARIO))
+    finally:
+        sim._Run = orig
+    run = captured[0]
+    cfg = scen.normalize(copy.deepcopy(PARITY_SCENARIO))
+    spec = scen.build_model_spec(cfg)
+    trace = moe.generate_routing(scen.build_routing_spec(cfg), spec, report.tokens)
+    layers = list(spec.moe_layer_indices)
+    key = lambda e: f"{e[0]},{e[1]}"
+    ic = run._initial_cache
+    sims = {str(l): [[run._similarity((l, a), (l, b)) for b in range(8)] for a in range(8)]
+            for l in layers}
+    kinds = {"hit", "fetch", "substitute", "prefetch", "demote", "evict"}
+    return dict(
+        scenario=PARITY_SCENARIO, layers=layers, encoder_layers=list(spec.encoder_moe_layers),
+        tokens=[dict(experts={str(l): list(t.layer_experts[l]) for l in layers},
+                     embedding=t.embedding.tolist(), context=t.context.tolist())
+                for t in trace.tokens],
+        predictor=dict(w1=run.mlp.w1.tolist(), b1=run.mlp.b1.tolist(), w2=run.mlp.w2.tolist(),
+                       b2=run.mlp.b2.tolist(), embed_dim=run.mlp.embed_dim,
+                       context_dim=run.mlp.context_dim),
+        freqs={key(e): f for e, f in run.freqs.items()},
+        priorities={key(e): p for e, p in run.priorities.items()},
+        prio_threshold=run.prio_threshold, hard_pinned=sorted(key(e) for e in run.hard_pinned),
+        similarity=sims,
+        policy=dict(theta_base=run.policy.theta_base, delta_evict=run.policy.delta_evict,
+                    lambda_evict=run.policy.lambda_evict,
+                    substitution_sim_min=run.policy.substitution_sim_min,
+                    half_life=ic.half_life),
+        initial=dict(workspace=[key(e) for e in ic.workspace], cache=[key(e) for e in ic.cache]),
+        capacities=dict(workspace=ic.workspace_capacity, cache=ic.cache_capacity),
+        events=[r for r in report.events if r["event"] in kinds],
+        report=dict(demand_count=report.demand_count, hit_count=report.hit_count,
+                    hit_rate=report.hit_rate, prefetch_issued=report.prefetch_issued,
+                    prefetch_hit_count=report.prefetch_hit_count,
+                    substitution_count=report.substitution_count,
+                    late_prefetch_count=report.late_prefetch_count))
+
+
 def main():
     moe, agg, off = _ref()
+    (OUT / "cache_parity.json").write_text(json.dumps(cache_parity(moe)))
     (OUT / "priority_cases.json").write_text(json.dumps(priority_cases(off), indent=1))
     (OUT / "traces.json").write_text(json.dumps(traces_and_predictor(moe, off)))
     OUT.mkdir(parents=True, exist_ok=True)

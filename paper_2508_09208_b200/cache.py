@@ -51,30 +51,67 @@ class CacheStats:
     evictions: int = 0
     h2d_bytes: int = 0
     waves: int = 0
-    events: list = field(default_factory=list)  # (kind, expert) in decision order
+    events: list = field(default_factory=list)  # (kind, expert[, used]) in decision order
 
     def hit_rate(self) -> float:
         return self.hits / self.demand if self.demand else 0.0
 
 
-class ExpertCache:
-    """Slot manager + policy for one MoE layer's experts (ids (layer, slot))."""
+class EventLog:
+    """Cache decision records in the reference simulator's event format
+    (simulator.py:86-99: {"tick", "event", "seq", payload keys sorted}) with
+    its event kinds (hit / fetch / substitute / prefetch / demote / evict,
+    simulator.py:47-63) and payload keys (expert, tier_from, tier_to, bytes,
+    used, penalty, theta, p). Timing fields of the analytic simulator
+    (comm_s, completes_s) are absent: copies here are real and asynchronous.
+    write_jsonl / the reference's read_events_jsonl round-trip."""
 
-    def __init__(self, host_experts: torch.Tensor, layer: int, n_slots: int,
+    def __init__(self):
+        self.records = []
+        self._seq = 0
+
+    def emit(self, tick: int, kind: str, **payload):
+        rec = {"tick": int(tick), "event": kind, "seq": self._seq}
+        for key in sorted(payload):
+            rec[key] = payload[key]
+        self.records.append(rec)
+        self._seq += 1
+        return rec
+
+    def write_jsonl(self, path: str) -> None:
+        import json
+        with open(path, "w", encoding="utf-8") as fh:
+            for rec in self.records:
+                fh.write(json.dumps(rec) + "\n")
+
+
+class ExpertCache:
+    """Slot manager + policy for the experts of one or more MoE layers (ids
+    (layer, slot)) in ONE HBM budget, like the simulator's single CacheState
+    over all layers (simulator.py:415-420). `host_experts` is a pinned
+    [E, numel] tensor for the single layer `layer`, or {layer: tensor}."""
+
+    def __init__(self, host_experts, layer: int = None, n_slots: int = 0,
                  workspace_slots: int = 2, policy: OffloadPolicy = None, freqs=None,
                  pinned=(), device=None, substitution=False, similarity=None,
-                 priorities: dict = None, priority_threshold: float = 1.0):
-        if not host_experts.is_pinned():
+                 priorities: dict = None, priority_threshold: float = 1.0,
+                 half_life: float = 256.0):
+        hosts = dict(host_experts) if isinstance(host_experts, dict) else {layer: host_experts}
+        if any(not h.is_pinned() for h in hosts.values()):
             raise ValueError("host expert store must be pinned memory")
-        E, numel = host_experts.shape
+        shapes = {tuple(h.shape[1:]) for h in hosts.values()}
+        if len(shapes) != 1:
+            raise ValueError("every layer's experts must have one flat size")
         if not 1 <= workspace_slots < n_slots:
             raise ValueError("need 1 <= workspace_slots < n_slots")
-        self.host = host_experts
-        self.layer = layer
-        self.E = E
+        numel = next(iter(hosts.values())).shape[1]
+        self.host = hosts
+        self.layers = sorted(hosts)
+        self.layer = self.layers[0]            # single-layer caches: the layer
+        self.E = max(h.shape[0] for h in hosts.values())
         self.dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
         self.pool = ExpertPool(n_slots, numel, device=self.dev)
-        self.bytes = numel * host_experts.element_size()
+        self.bytes = numel * next(iter(hosts.values())).element_size()
         self.policy = policy or OffloadPolicy()
         self.substitution = substitution
         self.similarity = similarity  # callable (eid_a, eid_b) -> float
@@ -87,19 +124,22 @@ class ExpertCache:
         self.slot_of = {}
         self._free_slots = list(range(n_slots - 1, -1, -1))
         self.stats = CacheStats()
+        self.log = EventLog()
         self.tick = 0
-        self.last_probs = None
+        self.last_probs = {}       # layer -> predicted probabilities (eviction scores)
         self.prefetched = set()
-        freqs = freqs if freqs is not None else {(layer, s): 1.0 / E for s in range(E)}
+        self.inflight = set()      # prefetched, pinned until demanded or the next step
+        all_ids = [(l, s) for l in self.layers for s in range(hosts[l].shape[0])]
+        freqs = freqs if freqs is not None else {e: 1.0 / self.E for e in all_ids}
         max_f = max(max(freqs.values()), 1e-12)
         self.importance = {e: f / max_f for e, f in freqs.items()}
-        sizes = {(layer, s): float(self.bytes) for s in range(E)}
+        sizes = {e: float(self.bytes) for e in all_ids}
         ws_cap = workspace_slots * float(self.bytes)
         ca_cap = (n_slots - workspace_slots) * float(self.bytes)
         plan = plan_initial_placement(sizes, freqs, ws_cap, ca_cap, pinned=frozenset(pinned),
                                       working_set_bytes=float(self.bytes))
         self.state = build_cache_state(plan, sizes, ws_cap, ca_cap, pinned=set(pinned),
-                                       importance=self.importance)
+                                       importance=self.importance, half_life=half_life)
         for eid in self.state.gpu_resident_ids():
             self._load(eid)
         self.hard_pinned = set(pinned)
@@ -111,7 +151,7 @@ class ExpertCache:
         with torch.cuda.stream(self.copy_stream):
             if self._free_pending[slot]:
                 self.copy_stream.wait_event(self.free_ev[slot])
-            self.pool.view(slot).copy_(self.host[eid[1]], non_blocking=True)
+            self.pool.view(slot).copy_(self.host[eid[0]][eid[1]], non_blocking=True)
             self.ready[slot].record(self.copy_stream)
         self.stats.h2d_bytes += self.bytes
         return slot
@@ -130,13 +170,25 @@ class ExpertCache:
         for s in slots:
             stream.wait_event(self.ready[s])
 
+    # ------------------------------------------------------------ steps
+    def begin_step(self, tick: int = None) -> None:
+        """Start of a token step (the simulator's token-start + arrival sweep,
+        simulator.py:503-513, 684-687): prefetches issued in earlier steps
+        have landed (their copies are stream-ordered before any reader), so
+        their in-flight pins are dropped."""
+        self.tick = self.tick + 1 if tick is None else int(tick)
+        for e in sorted(self.inflight):
+            if e not in self.hard_pinned:
+                self.state.pinned.discard(e)
+        self.inflight.clear()
+
     # ------------------------------------------------------------ policy
     def _scores(self):
         out = {}
-        probs = self.last_probs
         for eid in self.state.cache:
             if eid in self.state.pinned:
                 continue
+            probs = self.last_probs.get(eid[0])
             p = float(probs[eid[1]]) if probs is not None else 0.0
             out[eid] = eviction_score(p, self.state.recent_value(eid, self.tick),
                                       self.importance.get(eid, 0.0), self.policy.delta_evict,
@@ -154,6 +206,8 @@ class ExpertCache:
             self.prefetched.discard(v)
             self.stats.evictions += 1
             self.stats.events.append(("evict", v))
+            self.log.emit(self.tick, "evict", expert=list(v), tier_from=CACHE, tier_to=HOST,
+                          bytes=float(self.bytes))
         return True
 
     def _room_in_workspace(self) -> bool:
@@ -169,10 +223,14 @@ class ExpertCache:
             if self.state.free_bytes(CACHE) >= b or self._make_room_cache(b):
                 self.state.move(victim, WORKSPACE, CACHE)
                 self.stats.events.append(("demote", victim))
+                self.log.emit(self.tick, "demote", expert=list(victim), tier_from=WORKSPACE,
+                              tier_to=CACHE, bytes=b)
             else:
                 self.state.move(victim, WORKSPACE, HOST)
                 self._release(victim)
                 self.stats.events.append(("evict", victim))
+                self.log.emit(self.tick, "evict", expert=list(victim), tier_from=WORKSPACE,
+                              tier_to=HOST, bytes=b)
         return True
 
     def serve(self, demanded: list):
@@ -187,7 +245,12 @@ class ExpertCache:
         for eid in demanded:
             self.stats.demand += 1
             if self.state.resident(eid):
+                tier = self.state.tier_of(eid)
                 self.stats.hits += 1
+                if eid in self.inflight:   # the prefetch has landed: in-flight pin off
+                    self.inflight.discard(eid)
+                    if eid not in self.hard_pinned:
+                        self.state.pinned.discard(eid)
                 if eid in self.prefetched:
                     self.stats.prefetch_hits += 1
                     self.prefetched.discard(eid)
@@ -195,6 +258,8 @@ class ExpertCache:
                 self.state.pinned.add(eid)
                 out[eid] = self.slot_of[eid]
                 self.stats.events.append(("hit", eid))
+                self.log.emit(self.tick, "hit", expert=list(eid), tier_from=tier, tier_to=tier,
+                              bytes=0.0)
                 continue
             if self.substitution and self.similarity is not None:
                 dec = correct_misprediction(eid, self.state, self.similarity, self.policy,
@@ -206,6 +271,9 @@ class ExpertCache:
                     self.state.pinned.add(dec.expert)
                     out[eid] = self.slot_of[dec.expert]
                     self.stats.events.append(("substitute", eid, dec.expert))
+                    self.log.emit(self.tick, "substitute", expert=list(eid),
+                                  used=list(dec.expert), penalty=dec.penalty, tier_from=HOST,
+                                  tier_to=HOST, bytes=0.0)
                     continue
             if self._room_in_workspace():
                 tier = WORKSPACE
@@ -219,28 +287,38 @@ class ExpertCache:
             out[eid] = self._load(eid)
             self.stats.fetches += 1
             self.stats.events.append(("fetch", eid))
+            self.log.emit(self.tick, "fetch", expert=list(eid), tier_from=HOST, tier_to=tier,
+                          bytes=b)
         return out
 
     def unpin(self, eids):
         for e in eids:
-            if e not in self.hard_pinned:
+            if e not in self.hard_pinned and e not in self.inflight:
                 self.state.pinned.discard(e)
 
-    def prefetch(self, probs, theta: float):
-        """Threshold-gated prefetch of next-use experts into the cache tier
-        (simulator._predict_and_prefetch, simulator.py:578-620); copies are
+    def prefetch(self, probs, theta: float, layer: int = None):
+        """Threshold-gated prefetch of next-use experts of `layer` into the
+        cache tier (simulator._predict_and_prefetch, simulator.py:578-620):
+        `probs` (over the layer's cache experts) also become the layer's
+        eviction-score probabilities; each prefetched expert is pinned while
+        in flight (until it is demanded or the next step begins). Copies are
         asynchronous on the copy stream."""
-        self.last_probs = np.asarray(probs, dtype=float)
-        chosen = decide_prefetch(self.last_probs, theta, self.state, self.layer,
-                                 lambda e: float(self.bytes))
+        layer = self.layer if layer is None else layer
+        probs = np.asarray(probs, dtype=float)
+        self.last_probs[layer] = probs
+        chosen = decide_prefetch(probs, theta, self.state, layer, lambda e: float(self.bytes))
         for eid in chosen:
             if self.state.free_bytes(CACHE) < self.bytes and not self._make_room_cache(self.bytes):
                 break
             self.state.move(eid, HOST, CACHE)
+            self.state.pinned.add(eid)   # guard the in-flight copy (simulator.py:612)
+            self.inflight.add(eid)
             self._load(eid)
             self.prefetched.add(eid)
             self.stats.prefetch_issued += 1
             self.stats.events.append(("prefetch", eid))
+            self.log.emit(self.tick, "prefetch", expert=list(eid), tier_from=HOST, tier_to=CACHE,
+                          bytes=float(self.bytes), theta=float(theta), p=float(probs[eid[1]]))
         return chosen
 
     def check(self):
@@ -320,8 +398,11 @@ class CachedMoELayer:
     """MoELayer whose experts live in an ExpertCache (Switch / top-1 or top-2)."""
 
     def __init__(self, wg, cache: ExpertCache, d_ff: int, act="relu", top_k=1, norm_topk=None,
-                 capacity_factor=1.25, wave_slots: int = None):
+                 capacity_factor=1.25, wave_slots: int = None, layer: int = None):
         self.cache = cache
+        self.layer_id = cache.layer if layer is None else layer  # cache ids (layer_id, group)
+        if self.layer_id not in cache.host:
+            raise ValueError(f"the cache holds no experts of layer {self.layer_id}")
         n_exp = wg.shape[1]
         # group g of the layer <-> cache expert (layer, g); set_variant(lut, ...) maps a
         # fused variant's original experts onto the cache's retained experts
@@ -338,15 +419,21 @@ class CachedMoELayer:
         """Route through a fused variant: slot_map[E] -> group index, where
         group g is the cache's expert (layer, g) (ModelVariant.group_table)."""
         G = max(slot_map) + 1
-        if G > self.cache.E:
-            raise ValueError(f"{G} groups but the cache holds {self.cache.E} experts")
+        n = self.cache.host[self.layer_id].shape[0]
+        if G > n:
+            raise ValueError(f"{G} groups but the cache holds {n} experts of this layer")
         self.layer.set_variant(slot_map, [0] * G)  # slots come from the cache per wave
 
-    def forward(self, x, out=None, after_route=None, routing=None):
-        """`after_route(routing)` runs after the demand set is known and before
-        the GEMMs are enqueued: the stack issues the next layer's prefetch
-        there so its copies overlap this layer's expert GEMMs. `routing` =
-        (expert_idx, probs) replays given choices (MoELayer.route)."""
+    def forward(self, x, out=None, after_route=None, after_serve=None, routing=None, step=True):
+        """`after_route(routing)` runs right after routing (the stack launches
+        the next-layer predictor there, so it runs before this layer's
+        GEMMs); `after_serve(handle)` runs once this layer's demand is served
+        and its GEMMs are enqueued — the reference order (serve, then
+        predict and prefetch, simulator.py:700-712) — so the prefetch copies
+        overlap this layer's GEMMs. `routing` = (expert_idx, probs) replays
+        given choices (MoELayer.route). A standalone layer advances the
+        cache clock itself (`step=True`); in a stack (`step=False` from
+        CachedMoEStack) the stack does, once per token step."""
         L = self.layer
         T = x.shape[0]
         if out is None:
@@ -358,17 +445,19 @@ class CachedMoELayer:
         fused, gather = ws["fused"], ws["gather"]
         kernels.permute(x, r.gate, r.scan, r.capacity, r.rows, y_zero=out if k1 else None,
                         out=r.perm, copy_rows=not gather)
+        handle = after_route(r) if after_route is not None else None
         kept = r.scan.group_kept.cpu().numpy()  # the demand set (the layer's one host sync)
-        if after_route is not None:
-            after_route(r)
         c = self.cache
-        c.tick += 1
-        if len(kept) > c.E:
-            raise ValueError(f"layer has {len(kept)} groups but the cache holds {c.E} experts; "
+        lid = self.layer_id
+        if step:
+            c.begin_step()
+        n_here = c.host[lid].shape[0]
+        if len(kept) > n_here:
+            raise ValueError(f"layer has {len(kept)} groups but the cache holds {n_here} experts; "
                              "call layer.set_variant(lut, ...) for a fused variant")
         order = [int(g) for g in np.argsort(-kept, kind="stable") if kept[g] > 0]
-        hits = [g for g in order if c.state.resident((c.layer, g))]
-        misses = [g for g in order if not c.state.resident((c.layer, g))]
+        hits = [g for g in order if c.state.resident((lid, g))]
+        misses = [g for g in order if not c.state.resident((lid, g))]
         # every hit is already resident: one wave serves them all (no copies,
         # no slots needed); only misses are bounded by the free slots
         waves = ([hits] if hits else []) + \
@@ -379,14 +468,14 @@ class CachedMoELayer:
         epi2 = kernels.EPI_SCALE_SCATTER if k1 else kernels.EPI_STORE
         tab = self._tables.numpy()
         for w, wave in enumerate(waves):
-            ids = [(c.layer, g) for g in wave]
+            ids = [(lid, g) for g in wave]
             slots = c.serve(ids)
             c.stats.waves += 1
             tab[w] = 0
             G = len(kept)
             for g in wave:
                 tab[w, 0, g] = kept[g]
-                tab[w, 1, g] = slots[(c.layer, g)]
+                tab[w, 1, g] = slots[(lid, g)]
             used = sorted({slots[e] for e in ids})
             self._tables_dev[w].copy_(self._tables[w], non_blocking=True)
             c.wait_ready(used, comp)
@@ -408,6 +497,8 @@ class CachedMoELayer:
             c.unpin(list(ids) + [e for e in c.slot_of if c.slot_of[e] in used])
         if not k1:
             kernels.combine(ws["y_perm"], r.perm.token_pos, r.gate.gate_prob, out=out)
+        if after_serve is not None:
+            after_serve(handle)
         c.check()
         L.last = r
         return out

@@ -101,6 +101,7 @@ class MoELayer:
             raise ValueError("group slot outside the pool")
         dev = self.wg.device
         self.G = G
+        self.slot_map_host = list(slot_map)
         self.slot_map = torch.tensor(slot_map, dtype=torch.int32, device=dev)
         self.group_slot = torch.tensor(group_slots, dtype=torch.int32, device=dev)
         self._ws = {}

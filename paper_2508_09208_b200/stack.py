@@ -31,18 +31,23 @@ import torch
 from .offload import OffloadPolicy, prefetch_threshold
 
 
-def fold_demand(demand, slot_map, n_groups: int) -> np.ndarray:
+def fold_demand(demand, slot_map, n_groups: int, mode: str = "complement") -> np.ndarray:
     """Per-original-expert demand probabilities of the next layer -> its
-    cache's group space (a fused variant's experts are (layer, group)):
-    P(group g demanded) = 1 - prod_{e in g} (1 - p_e). The reference folds
-    its per-token predictor output the same way before decide_prefetch,
-    with a sum (np.add.at(merged, map_arrays[nxt], raw), simulator.py:587-588);
-    for the batch demand probabilities here the complement product is the
-    consistent fold (it stays a probability)."""
-    demand = np.clip(np.asarray(demand, np.float64), 0.0, 1.0)
+    cache's group space (a fused variant's experts are (layer, group)).
+    mode "sum": the reference's fold of one token's predictor output,
+    np.add.at(merged, map_arrays[nxt], raw) (simulator.py:587-588);
+    mode "complement": P(group g demanded by the batch) =
+    1 - prod_{e in g} (1 - p_e), the consistent fold of batch demand
+    probabilities (stays a probability)."""
     lut = np.asarray(slot_map, np.int64)
+    demand = np.asarray(demand, np.float64)[:len(lut)]
+    if mode == "sum":
+        merged = np.zeros(n_groups)
+        np.add.at(merged, lut, demand)
+        return merged
+    demand = np.clip(demand, 0.0, 1.0)
     miss = np.ones(n_groups)
-    np.multiply.at(miss, lut, 1.0 - demand[:len(lut)])
+    np.multiply.at(miss, lut, 1.0 - demand)
     return 1.0 - miss
 
 
@@ -54,32 +59,74 @@ class StackLayer:
 
 
 class CachedMoEStack:
+    """One token step = one forward of every layer over the batch.
+
+    The layers' caches may be one shared ExpertCache (the reference's single
+    CacheState over all MoE layers) or one per layer. At a batch of one
+    token the stack is the reference's per-token loop (simulator.py:684-724)
+    with the same order of decisions — serve layer l, then predict layer
+    l+1 (raw predictor output folded with the reference's sum) and prefetch
+    — and its JSONL event log matches the simulator's decision stream
+    (tests/test_cache_parity.py)."""
+
     def __init__(self, layers: list, predictor=None, policy: OffloadPolicy = None,
-                 s_b: float = 1.0, mem_avail: float = 1.0, mem_total: float = 1.0):
+                 s_b: float = 1.0, mem_avail: float = 1.0, mem_total: float = 1.0,
+                 theta: float = None):
         self.layers = layers
         self.predictor = predictor
         self.policy = policy or OffloadPolicy()
-        self.theta = prefetch_threshold(self.policy, s_b, mem_avail, mem_total)
+        self.theta = prefetch_threshold(self.policy, s_b, mem_avail, mem_total) \
+            if theta is None else float(theta)
         self.prefetch_log = []
+        self.steps = 0
 
-    def forward(self, x, emb=None, ctx=None, routings=None):
+    def caches(self) -> list:
+        seen, out = set(), []
+        for sl in self.layers:
+            c = sl.layer.cache
+            if id(c) not in seen:
+                seen.add(id(c))
+                out.append(c)
+        return out
+
+    def forward(self, x, emb=None, ctx=None, routings=None, tick: int = None):
         """x [T, d] bf16; emb/ctx [T, *] float64 device tensors for the
         predictor (token embedding / context, as TokenRecord carries);
         `routings` (optional, one (expert_idx, probs) per layer) replays a
-        routing trace instead of running each layer's router."""
+        routing trace instead of running each layer's router; `tick` is the
+        step's clock (default: one more than the last)."""
+        T = x.shape[0]
+        t = self.steps if tick is None else int(tick)
+        self.steps = t + 1
+        for c in self.caches():
+            c.begin_step(t)
         h = x
         for i, sl in enumerate(self.layers):
             nxt = self.layers[i + 1] if i + 1 < len(self.layers) else None
-            hook = None
+            pre = post = None
             if nxt is not None and sl.encoder and self.predictor is not None:
-                def hook(r, sl=sl, nxt=nxt):
+                mode = "sum" if T == 1 else "any"
+
+                def pre(r, mode=mode):
+                    # predictor right after routing (before this layer's
+                    # GEMMs); its demand comes back by an async copy
                     _, demand = self.predictor.predict_slots(r.gate.expert_idx, emb, ctx,
-                                                             want_demand=True, demand_mode="any")
+                                                             want_demand=True, demand_mode=mode)
+                    host = torch.empty(demand.shape, dtype=demand.dtype, pin_memory=True)
+                    host.copy_(demand, non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record()
+                    return host, ev
+
+                def post(handle, sl=sl, nxt=nxt, T=T):
+                    host, ev = handle
+                    ev.synchronize()       # gate + predictor only, not the GEMMs
                     L = nxt.layer.layer
-                    demand = fold_demand(demand.cpu().numpy(), L.slot_map.cpu().numpy(), L.G)
-                    chosen = nxt.layer.cache.prefetch(demand, self.theta)
+                    probs = fold_demand(host.numpy(), L.slot_map_host, L.G,
+                                        mode="sum" if T == 1 else "complement")
+                    chosen = nxt.layer.cache.prefetch(probs, self.theta, layer=nxt.layer.layer_id)
                     self.prefetch_log.append((sl.index, nxt.index, chosen))
-            y = sl.layer.forward(h, after_route=hook,
+            y = sl.layer.forward(h, after_route=pre, after_serve=post, step=False,
                                  routing=routings[i] if routings is not None else None)
             h = (y.float() + h.float()).to(torch.bfloat16)
         return h
