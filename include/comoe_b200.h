@@ -72,6 +72,28 @@ int comoe_gate_topk(const void* x, int T, int d, const void* wg_split, int E, in
                     int* expert_idx, int* group_idx, float* gate_prob, int* local_rank,
                     int* tile_hist, void* stream);
 
+/* comoe_gate_route: comoe_gate_topk and comoe_route_scan in ONE launch
+ * (the router with capacity masking as one kernel). The gate epilogue
+ * stores each 128-token tile's group histogram; after the last tile the
+ * persistent (co-resident) grid meets at a device-side barrier, each CTA
+ * scans whole histogram columns in stream order, and the last CTA to finish
+ * writes group_count /
+ * group_kept / group_base. Outputs are identical to comoe_gate_topk followed
+ * by comoe_route_scan (tile_offset[k][ntiles][G] included; tile_hist is not
+ * written). `workspace` (comoe_gate_route_workspace_bytes, 16-byte aligned)
+ * must be zero-filled once before its first use and is then
+ * self-maintaining (a device-side epoch advances per launch, so CUDA-graph
+ * replays need no reset); one workspace per concurrently running launch.
+ * Replaces the routing source generate_routing (pkg/src/comoe/moe.py:186-230)
+ * and the per-expert counts of collect_stats (moe.py:250-262).
+ */
+long comoe_gate_route_workspace_bytes(int T, int top_k, int n_groups);
+int comoe_gate_route(const void* x, int T, int d, const void* wg_split, int E, int top_k,
+                     int norm_topk, const int* slot_map, int n_groups, int capacity,
+                     float* logits_out, int* expert_idx, int* group_idx, float* gate_prob,
+                     int* local_rank, int* tile_offset, int* group_count, int* group_kept,
+                     int* group_base, void* workspace, void* stream);
+
 /* Replayed routing: the tables comoe_gate_topk produces after top-k, from
  * given expert choices expert_idx[T,k] (a reference RoutingTrace,
  * pkg/src/comoe/moe.py:146-162, or any external router) and optional

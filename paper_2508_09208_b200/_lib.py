@@ -28,6 +28,9 @@ _SIGNATURES = {
     "comoe_gate_prepare": [_p, _c_int, _c_int, _p, _p],
     "comoe_gate_topk": [_p, _c_int, _c_int, _p, _c_int, _c_int, _c_int, _p, _c_int, _p,
                         _p, _p, _p, _p, _p, _p],
+    "comoe_gate_route_workspace_bytes": [_c_int, _c_int, _c_int],
+    "comoe_gate_route": [_p, _c_int, _c_int, _p, _c_int, _c_int, _c_int, _p, _c_int, _c_int,
+                         _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p],
     "comoe_route_from_indices": [_p, _p, _c_int, _c_int, _c_int, _p, _c_int, _p, _p, _p, _p, _p],
     "comoe_route_scan": [_p, _c_int, _c_int, _c_int, _c_int, _p, _p, _p, _p, _p],
     "comoe_expert_histogram": [_p, _c_long, _c_int, _p, _p],
@@ -66,7 +69,8 @@ _SIGNATURES = {
 }
 _RESTYPES = {"comoe_last_error": ctypes.c_char_p, "comoe_sim_workspace_bytes": _c_long,
              "comoe_ipc_handle_size": _c_int,
-             "comoe_predictor_workspace_bytes": _c_long}
+             "comoe_predictor_workspace_bytes": _c_long,
+             "comoe_gate_route_workspace_bytes": _c_long}
 
 EXPORTED = tuple(_SIGNATURES)
 

@@ -58,7 +58,134 @@ struct GateParams {
   int* local_rank;      // [T, k]
   int* tile_hist;       // [k][ntiles][G]
   int debug;            // dev attribution (COMOE_GATE_DEBUG): 1 no router loads, 2 x from tile 0, 4 no x loads
+  // Folded capacity scan (comoe_gate_route; lb == null: histograms only).
+  // The epilogue stores each tile's group histogram group-major and adds it
+  // to the per-group totals; after the last tile every CTA meets at a grid
+  // barrier (the persistent grid is co-resident), scans whole histogram
+  // columns into stream-order tile offsets, and one CTA turns the totals
+  // into count / kept / base. A device-side epoch advances once per launch
+  // and selects the parity of the barrier counter and totals, which that
+  // launch zeroes for the next one: the workspace is zero-filled once and
+  // never reset again (CUDA-graph replays included).
+  int* lb;                // [G][k * ntiles] histograms, group-major
+  unsigned int* lb_ctrl;  // [0] epoch of the last completed launch, [2 + parity] barrier arrivals
+  int* lb_total;          // [2 parities][kGateMaxE] assignments per group
+  int* tile_offset;       // [k][ntiles][G] exclusive stream-order prefix
+  int* group_count;       // [G]
+  int* group_kept;        // [G]
+  int* group_base;        // [G]
+  int capacity;
 };
+
+// ------------------------------------------------------------ folded scan
+// Publish one tile's histogram entry: group-major plus the running total for
+// the folded scan, the [k][ntiles][G] histogram for comoe_gate_topk +
+// comoe_route_scan.
+__device__ __forceinline__ void gate_publish_hist(const GateParams& p, int j, int tile, int g,
+                                                  int h, uint32_t ep) {
+  if (p.lb) {
+    p.lb[static_cast<long>(g) * p.top_k * p.ntiles + static_cast<long>(j) * p.ntiles + tile] = h;
+    if (h) atomicAdd(p.lb_total + (ep & 1u) * kGateMaxE + g, h);
+  } else {
+    p.tile_hist[(static_cast<long>(j) * p.ntiles + tile) * p.G + g] = h;
+  }
+}
+
+__device__ __forceinline__ unsigned int ld_acquire_gpu_u32(const unsigned int* a) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_gpu_add(unsigned int* a, unsigned int v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+
+constexpr int kFoldPer = 4;  // histogram entries per thread loaded before the scan
+
+// After the main loop (all kGateThreads threads of every CTA): grid barrier,
+// column scans in stream order (all first choices in token order, then all
+// second choices), and count / kept / base from the per-group totals. Same
+// results as route_scan_coop below.
+__device__ __forceinline__ void gate_fold_scan(const GateParams& p, uint32_t ep) {
+  __shared__ int warp_tot[kGateThreads / 32];
+  unsigned int* arrivals = p.lb_ctrl + 2 + (ep & 1u);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();  // the CTA's histogram stores and totals, before the arrival
+    red_release_gpu_add(arrivals, 1u);
+    while (ld_acquire_gpu_u32(arrivals) < gridDim.x) {
+    }
+  }
+  __syncthreads();
+  const int S = p.top_k * p.ntiles;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  constexpr int nw = kGateThreads / 32;
+  // the CTA that finalises the totals: the last one when it has no column
+  const int fin = static_cast<int>(gridDim.x) > p.G ? static_cast<int>(gridDim.x) - 1 : 0;
+  if (static_cast<int>(blockIdx.x) == fin) {
+    if (threadIdx.x < 128) {
+      const int g = threadIdx.x;
+      const int cnt = g < p.G ? __ldcg(p.lb_total + (ep & 1u) * kGateMaxE + g) : 0;
+      const int kept = min(cnt, p.capacity);
+      int v = kept;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int n = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += n;
+      }
+      if (lane == 31) warp_tot[w] = v;
+      named_bar_sync(1, 128);
+      int base = v - kept;
+      for (int i = 0; i < w; ++i) base += warp_tot[i];
+      if (g < p.G) {
+        p.group_count[g] = cnt;
+        p.group_kept[g] = kept;
+        p.group_base[g] = base;
+      }
+      // the next launch's totals and barrier start from zero
+      p.lb_total[((ep + 1u) & 1u) * kGateMaxE + g] = 0;
+      if (g == 0) {
+        p.lb_ctrl[2 + ((ep + 1u) & 1u)] = 0u;
+        p.lb_ctrl[0] = ep;
+      }
+    }
+    __syncthreads();
+  }
+  for (int g = blockIdx.x; g < p.G; g += gridDim.x) {
+    const int* col = p.lb + static_cast<long>(g) * S;
+    int carry = 0;
+    for (int b0 = 0; b0 < S; b0 += kFoldPer * kGateThreads) {
+      int x[kFoldPer];
+#pragma unroll
+      for (int c = 0; c < kFoldPer; ++c) {  // every load in flight before the scan
+        const int s = b0 + c * kGateThreads + threadIdx.x;
+        x[c] = s < S ? __ldcg(col + s) : 0;
+      }
+#pragma unroll
+      for (int c = 0; c < kFoldPer; ++c) {
+        if (b0 + c * kGateThreads >= S) break;
+        const int s = b0 + c * kGateThreads + threadIdx.x;
+        int v = x[c];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int n = __shfl_up_sync(0xffffffffu, v, o);
+          if (lane >= o) v += n;
+        }
+        if (lane == 31) warp_tot[w] = v;
+        __syncthreads();
+        int wb = 0, tot = 0;
+#pragma unroll
+        for (int i = 0; i < nw; ++i) {
+          if (i < w) wb += warp_tot[i];
+          tot += warp_tot[i];
+        }
+        if (s < S) p.tile_offset[static_cast<long>(s) * p.G + g] = carry + wb + v - x[c];
+        carry += tot;
+        __syncthreads();
+      }
+    }
+  }
+}
 
 // kPair: CTA pair (cta_group::2, M = 256 tokens): each SM stages its own 128
 // tokens and half of every router term (EP/2 experts), cutting per-SM shared-
@@ -227,6 +354,8 @@ __global__ void __launch_bounds__(kGateThreads, 1)
   }
   pdl_wait();     // x / slot_map may come from the preceding kernel
   pdl_trigger();  // persistent grid: the next kernel may launch and wait
+  __shared__ uint32_t s_ep;
+  if (threadIdx.x == 0 && p.lb) s_ep = *reinterpret_cast<volatile unsigned int*>(p.lb_ctrl) + 1u;
   for (int e = threadIdx.x; e < kGateMaxE; e += blockDim.x)
     smap[e] = e < p.E ? (p.slot_map ? __ldg(p.slot_map + e) : e) : -1;
   tc_fence_before();
@@ -234,6 +363,7 @@ __global__ void __launch_bounds__(kGateThreads, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  const uint32_t ep = p.lb ? s_ep : 0u;
 
   if (p.debug & 64) {  // dev: prologue + epilogue of the kernel only
   } else if (warp == 0) {
@@ -478,7 +608,7 @@ __global__ void __launch_bounds__(kGateThreads, 1)
             int h = 0;
             if (g < kGateMaxE)
               for (int qq = 0; qq < 4; ++qq) h += cnt[(j * 4 + qq) * kGateMaxE + g];
-            p.tile_hist[(static_cast<long>(j) * p.ntiles + tile) * p.G + g] = h;
+            gate_publish_hist(p, j, tile, g, h, ep);
           }
     }
   } else if (warp >= 4) {
@@ -635,7 +765,7 @@ __global__ void __launch_bounds__(kGateThreads, 1)
             int h = 0;
             if (g < kGateMaxE)
               for (int qq = 0; qq < 4; ++qq) h += cnt[(j * 4 + qq) * kGateMaxE + g];
-            p.tile_hist[(static_cast<long>(j) * p.ntiles + tile) * p.G + g] = h;
+            gate_publish_hist(p, j, tile, g, h, ep);
           }
     }
   }
@@ -652,6 +782,7 @@ __global__ void __launch_bounds__(kGateThreads, 1)
     else
       tmem_dealloc<kTmemCols>(tmem_base);
   }
+  if (p.lb) gate_fold_scan(p, ep);  // folded capacity scan (comoe_gate_route)
 }
 
 template <int EP, bool kPair, int kTerms, int kStages>
@@ -670,9 +801,7 @@ static int launch_gate_stages(const CUtensorMap& tx, const CUtensorMap& tw, cons
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if constexpr (kPair) {
     const int units = (p.ntiles + 1) / 2;
-    const int pairs = units < sms / 2 ? units : sms / 2;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(2 * pairs);
     cfg.blockDim = dim3(kGateThreads);
     cfg.dynamicSmemBytes = S::kTotal;
     cfg.stream = stream;
@@ -682,6 +811,21 @@ static int launch_gate_stages(const CUtensorMap& tx, const CUtensorMap& tw, cons
     attrs[0].val.clusterDim.y = 1;
     attrs[0].val.clusterDim.z = 1;
     cfg.attrs = attrs;
+    // the persistent grid must be co-resident (the folded scan meets at a
+    // grid barrier): at most as many pairs as can be resident at once
+    static int max_pairs = -1;
+    if (max_pairs < 0) {
+      cfg.gridDim = dim3(sms);
+      cfg.numAttrs = 1;
+      int clusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) != cudaSuccess || clusters < 1) {
+        cudaGetLastError();
+        clusters = sms / 2;
+      }
+      max_pairs = clusters < sms / 2 ? clusters : sms / 2;
+    }
+    const int pairs = units < max_pairs ? units : max_pairs;
+    cfg.gridDim = dim3(2 * pairs);
     cfg.numAttrs = 1 + pdl_attr(&attrs[1]);
     cudaLaunchKernelEx(&cfg, kern, tx, tw, p);
     return check_launch("gate_kernel(pair)");
@@ -986,20 +1130,25 @@ int comoe_gate_prepare(const float* wg, int d, int E, void* wg_split, void* stre
   return check_launch("gate_split_kernel");
 }
 
-int comoe_gate_topk(const void* x, int T, int d, const void* wg_split, int E, int top_k,
-                    int norm_topk, const int* slot_map, int n_groups, float* logits_out,
-                    int* expert_idx, int* group_idx, float* gate_prob, int* local_rank,
-                    int* tile_hist, void* stream) {
-  using namespace comoe;
-  COMOE_REQUIRE(x && wg_split && expert_idx && group_idx && gate_prob && local_rank && tile_hist,
-                kBadArg, "gate_topk: null pointer");
-  COMOE_REQUIRE(T > 0, kBadArg, "gate_topk: T=%d", T);
-  COMOE_REQUIRE(top_k == 1 || top_k == 2, kUnsupportedShape, "gate_topk: top_k=%d not in {1,2}", top_k);
-  COMOE_REQUIRE(top_k <= E, kBadArg, "gate_topk: top_k > E");
+}  // extern "C"
+
+namespace comoe {
+// Shared launch path of comoe_gate_topk (histograms) and comoe_gate_route
+// (folded scan: p.lb set).
+static int gate_launch(const void* x, int T, int d, const void* wg_split, int E, int top_k,
+                       int norm_topk, const int* slot_map, int n_groups, float* logits_out,
+                       int* expert_idx, int* group_idx, float* gate_prob, int* local_rank,
+                       int* tile_hist, GateParams fold, cudaStream_t s) {
+  COMOE_REQUIRE(x && wg_split && expert_idx && group_idx && gate_prob && local_rank &&
+                    (tile_hist || fold.lb),
+                kBadArg, "gate: null pointer");
+  COMOE_REQUIRE(T > 0, kBadArg, "gate: T=%d", T);
+  COMOE_REQUIRE(top_k == 1 || top_k == 2, kUnsupportedShape, "gate: top_k=%d not in {1,2}", top_k);
+  COMOE_REQUIRE(top_k <= E, kBadArg, "gate: top_k > E");
   const int EP = comoe_gate_padded_experts(E);
-  COMOE_REQUIRE(EP > 0, kUnsupportedShape, "gate_topk: E=%d must be in [1,%d]", E, kGateMaxE);
-  COMOE_REQUIRE(d % 64 == 0, kUnsupportedShape, "gate_topk: d=%d must be a multiple of 64", d);
-  COMOE_REQUIRE(n_groups >= 1 && n_groups <= E, kBadArg, "gate_topk: n_groups=%d", n_groups);
+  COMOE_REQUIRE(EP > 0, kUnsupportedShape, "gate: E=%d must be in [1,%d]", E, kGateMaxE);
+  COMOE_REQUIRE(d % 64 == 0, kUnsupportedShape, "gate: d=%d must be a multiple of 64", d);
+  COMOE_REQUIRE(n_groups >= 1 && n_groups <= E, kBadArg, "gate: n_groups=%d", n_groups);
   const bool pair = gate_pair_enabled();
   CUtensorMap tx, tw;
   int rc = make_tmap_bf16_2d(&tx, x, T, d, kGemmBM);
@@ -1007,14 +1156,19 @@ int comoe_gate_topk(const void* x, int T, int d, const void* wg_split, int E, in
   // box rows: a whole term per CTA for the concatenated-terms pair kernel
   rc = make_tmap_bf16_2d(&tw, wg_split, 3ull * EP, d, pair ? (gate_terms() == 2 ? EP : EP / 2) : EP);
   if (rc) return rc;
-  GateParams p{T, d, E, top_k, norm_topk, n_groups, (T + kGemmBM - 1) / kGemmBM, slot_map,
-               logits_out, expert_idx, group_idx, gate_prob, local_rank, tile_hist, 0};
+  GateParams p = fold;
+  p.T = T; p.d = d; p.E = E; p.top_k = top_k; p.norm_topk = norm_topk; p.G = n_groups;
+  p.ntiles = (T + kGemmBM - 1) / kGemmBM;
+  p.slot_map = slot_map; p.logits = logits_out; p.expert_idx = expert_idx;
+  p.group_idx = group_idx; p.gate_prob = gate_prob; p.local_rank = local_rank;
+  p.tile_hist = tile_hist;
   static const int dbg = [] {
     const char* e = std::getenv("COMOE_GATE_DEBUG");
     return e ? std::atoi(e) : 0;
   }();
   p.debug = dbg;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  COMOE_REQUIRE(!(p.lb && dbg), kBadArg,
+                "gate_route: COMOE_GATE_DEBUG switches need comoe_gate_topk + comoe_route_scan");
   switch (EP) {
     case 16: return pair ? launch_gate<16, true>(tx, tw, p, s) : launch_gate<16, false>(tx, tw, p, s);
     case 32: return pair ? launch_gate<32, true>(tx, tw, p, s) : launch_gate<32, false>(tx, tw, p, s);
@@ -1022,8 +1176,52 @@ int comoe_gate_topk(const void* x, int T, int d, const void* wg_split, int E, in
     case 128: return pair ? launch_gate<128, true>(tx, tw, p, s) : launch_gate<128, false>(tx, tw, p, s);
     default: break;
   }
-  set_error("gate_topk: no kernel for EP=%d", EP);
+  set_error("gate: no kernel for EP=%d", EP);
   return kUnsupportedShape;
+}
+}  // namespace comoe
+
+extern "C" {
+
+int comoe_gate_topk(const void* x, int T, int d, const void* wg_split, int E, int top_k,
+                    int norm_topk, const int* slot_map, int n_groups, float* logits_out,
+                    int* expert_idx, int* group_idx, float* gate_prob, int* local_rank,
+                    int* tile_hist, void* stream) {
+  using namespace comoe;
+  COMOE_REQUIRE(tile_hist, kBadArg, "gate_topk: null pointer");
+  return gate_launch(x, T, d, wg_split, E, top_k, norm_topk, slot_map, n_groups, logits_out,
+                     expert_idx, group_idx, gate_prob, local_rank, tile_hist, GateParams{},
+                     static_cast<cudaStream_t>(stream));
+}
+
+long comoe_gate_route_workspace_bytes(int T, int top_k, int n_groups) {
+  const long nt = (static_cast<long>(T) + comoe::kGemmBM - 1) / comoe::kGemmBM;
+  return 16 + 8L * comoe::kGateMaxE + 4L * top_k * nt * n_groups;
+}
+
+int comoe_gate_route(const void* x, int T, int d, const void* wg_split, int E, int top_k,
+                     int norm_topk, const int* slot_map, int n_groups, int capacity,
+                     float* logits_out, int* expert_idx, int* group_idx, float* gate_prob,
+                     int* local_rank, int* tile_offset, int* group_count, int* group_kept,
+                     int* group_base, void* workspace, void* stream) {
+  using namespace comoe;
+  COMOE_REQUIRE(tile_offset && group_count && group_kept && group_base && workspace, kBadArg,
+                "gate_route: null pointer");
+  COMOE_REQUIRE(capacity >= 0, kBadArg, "gate_route: capacity=%d", capacity);
+  COMOE_REQUIRE((reinterpret_cast<uintptr_t>(workspace) & 15) == 0, kBadArg,
+                "gate_route: workspace must be 16-byte aligned");
+  GateParams f{};
+  f.lb_ctrl = static_cast<unsigned int*>(workspace);
+  f.lb_total = reinterpret_cast<int*>(static_cast<char*>(workspace) + 16);
+  f.lb = f.lb_total + 2 * kGateMaxE;
+  f.tile_offset = tile_offset;
+  f.group_count = group_count;
+  f.group_kept = group_kept;
+  f.group_base = group_base;
+  f.capacity = capacity;
+  return gate_launch(x, T, d, wg_split, E, top_k, norm_topk, slot_map, n_groups, logits_out,
+                     expert_idx, group_idx, gate_prob, local_rank, nullptr, f,
+                     static_cast<cudaStream_t>(stream));
 }
 
 int comoe_gate_num_tiles(int T) { return (T + comoe::kGemmBM - 1) / comoe::kGemmBM; }

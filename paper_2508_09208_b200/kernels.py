@@ -111,6 +111,48 @@ def gate_topk(x, wg_split, E, top_k, norm_topk, slot_map=None, n_groups=None,
     return out
 
 
+def gate_route_workspace(T: int, top_k: int, n_groups: int, device) -> torch.Tensor:
+    """Zero-filled look-back workspace of comoe_gate_route (status words +
+    a device-side epoch; self-maintaining after the zero fill)."""
+    n = int(_lib.load().comoe_gate_route_workspace_bytes(int(T), int(top_k), int(n_groups)))
+    return torch.zeros((n + 7) // 8, dtype=torch.int64, device=device)
+
+
+def gate_route(x, wg_split, E, top_k, norm_topk, capacity: int, workspace: torch.Tensor,
+               slot_map=None, n_groups=None, want_logits=False, out: GateOutput = None,
+               scan: "ScanOutput" = None):
+    """Gate + capacity scan in one launch (comoe_gate_route): the same
+    tables as gate_topk followed by route_scan, except tile_hist (unused)."""
+    _need(x, "x", torch.bfloat16, 2)
+    _need(wg_split, "wg_split", torch.bfloat16, 3)
+    T, d = x.shape
+    G = E if n_groups is None else int(n_groups)
+    if slot_map is not None:
+        _need(slot_map, "slot_map", torch.int32, 1)
+    nt = gate_num_tiles(T)
+    dev = x.device
+    need = int(_lib.load().comoe_gate_route_workspace_bytes(T, int(top_k), G))
+    if workspace.device != dev or workspace.numel() * workspace.element_size() < need:
+        raise ValueError(f"gate_route: workspace must hold {need} bytes on {dev}")
+    if out is None:
+        out = GateOutput(
+            expert_idx=torch.empty((T, top_k), dtype=torch.int32, device=dev),
+            group_idx=torch.empty((T, top_k), dtype=torch.int32, device=dev),
+            gate_prob=torch.empty((T, top_k), dtype=torch.float32, device=dev),
+            local_rank=torch.empty((T, top_k), dtype=torch.int32, device=dev),
+            tile_hist=None,
+            logits=torch.empty((T, E), dtype=torch.float32, device=dev) if want_logits else None)
+    if scan is None:
+        scan = ScanOutput(torch.empty((top_k, nt, G), dtype=torch.int32, device=dev),
+                          *(torch.empty(G, dtype=torch.int32, device=dev) for _ in range(3)))
+    _lib.call("comoe_gate_route", _ptr(x), T, d, _ptr(wg_split), E, top_k, int(norm_topk),
+              _ptr(slot_map), G, int(capacity), _ptr(out.logits), _ptr(out.expert_idx),
+              _ptr(out.group_idx), _ptr(out.gate_prob), _ptr(out.local_rank),
+              _ptr(scan.tile_offset), _ptr(scan.group_count), _ptr(scan.group_kept),
+              _ptr(scan.group_base), _ptr(workspace), _stream())
+    return out, scan
+
+
 def route_from_indices(expert_idx, E, probs=None, slot_map=None, n_groups=None,
                        out: GateOutput = None) -> GateOutput:
     """Routing tables from given expert choices (trace replay)."""

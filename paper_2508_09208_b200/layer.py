@@ -36,6 +36,14 @@ def _gather_enabled(act: str) -> bool:
         os.environ.get("COMOE_GATHER", "0") == "1"
 
 
+def _gate_fold() -> bool:
+    """Gate and capacity scan as one launch (comoe_gate_route, default).
+    COMOE_GATE_FOLD=0 runs comoe_gate_topk + comoe_route_scan (two
+    launches, identical tables)."""
+    return os.environ.get("COMOE_GATE_FOLD", "1") != "0" and \
+        os.environ.get("COMOE_GATE_DEBUG", "0") == "0"
+
+
 def _fused_gather() -> bool:
     """The fused FFN reads token rows straight from x with TMA gather4 (no
     permuted copy; default). COMOE_FUSED_GATHER=0 reads the permuted copy."""
@@ -154,6 +162,7 @@ class MoELayer:
                                        torch.empty(rows, dtype=torch.int32, device=dev),
                                        torch.empty(rows, dtype=torch.float32, device=dev),
                                        torch.empty((T, k), dtype=torch.int32, device=dev)),
+            lb=kernels.gate_route_workspace(T, k, self.G, dev) if _gate_fold() else None,
             h=None if fused else torch.empty((rows, self.d_ff), dtype=torch.bfloat16, device=dev),
             y_perm=torch.empty((rows, self.d), dtype=torch.bfloat16, device=dev) if k > 1 else None,
         )
@@ -181,9 +190,14 @@ class MoELayer:
             gate = kernels.GateOutput(gate.expert_idx, gate.group_idx, gate.gate_prob,
                                       gate.local_rank, gate.tile_hist,
                                       torch.empty((T, self.E), dtype=torch.float32, device=x.device))
-        kernels.gate_topk(x, self.wg_split, self.E, self.top_k, self.norm_topk,
-                          slot_map=self.slot_map, n_groups=self.G, out=gate)
-        kernels.route_scan(gate.tile_hist, ws["C"], out=ws["scan"])
+        if ws["lb"] is not None:
+            kernels.gate_route(x, self.wg_split, self.E, self.top_k, self.norm_topk, ws["C"],
+                               ws["lb"], slot_map=self.slot_map, n_groups=self.G, out=gate,
+                               scan=ws["scan"])
+        else:
+            kernels.gate_topk(x, self.wg_split, self.E, self.top_k, self.norm_topk,
+                              slot_map=self.slot_map, n_groups=self.G, out=gate)
+            kernels.route_scan(gate.tile_hist, ws["C"], out=ws["scan"])
         return LayerRouting(gate, ws["scan"], ws["perm"], ws["C"], ws["rows"])
 
     def forward(self, x: torch.Tensor, out: torch.Tensor = None,
@@ -245,9 +259,10 @@ class MoELayer:
 
     @property
     def kernels_per_forward(self) -> int:
-        """Device kernels one forward launches: gate, scan, permute, FFN (one
-        fused launch or two GEMMs) [, combine]."""
-        return (4 if self.fused else 5) + (0 if self.top_k == 1 else 1)
+        """Device kernels one forward launches: gate (+ scan unless folded),
+        permute, FFN (one fused launch or two GEMMs) [, combine]."""
+        return (3 if self.fused else 4) + (0 if _gate_fold() else 1) + \
+            (0 if self.top_k == 1 else 1)
 
     def capture(self, x: torch.Tensor, out: torch.Tensor = None) -> "CapturedForward":
         """Record one forward over the static buffers `x` (and `out`) as a

@@ -22,8 +22,21 @@ for _ in range(E):
     pool.alloc()
 layer = MoELayer(wg, pool, d_ff, act="relu", top_k=1, capacity_factor=1.25)
 ws = layer._workspace(T)
-run = lambda: kernels.gate_topk(x, layer.wg_split, E, 1, False, slot_map=layer.slot_map,
-                                n_groups=E, out=ws["gate"])
+mode = os.environ.get("MODE", "topk")  # topk | scan (topk + route_scan) | route (folded)
+lbw = kernels.gate_route_workspace(T, 1, E, dev)
+C = ws["C"]
+if mode == "route":
+    run = lambda: kernels.gate_route(x, layer.wg_split, E, 1, False, C, lbw,
+                                     slot_map=layer.slot_map, n_groups=E, out=ws["gate"],
+                                     scan=ws["scan"])
+elif mode == "scan":
+    def run():
+        kernels.gate_topk(x, layer.wg_split, E, 1, False, slot_map=layer.slot_map, n_groups=E,
+                          out=ws["gate"])
+        kernels.route_scan(ws["gate"].tile_hist, C, out=ws["scan"])
+else:
+    run = lambda: kernels.gate_topk(x, layer.wg_split, E, 1, False, slot_map=layer.slot_map,
+                                    n_groups=E, out=ws["gate"])
 flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
 reps = int(os.environ.get("REPS", "30"))
 run()
@@ -40,5 +53,5 @@ for _ in range(reps):
     ts.append(a.elapsed_time(b))
 ms = statistics.median(ts)
 ref = kernels.gate_topk(x, layer.wg_split, E, 1, False, slot_map=layer.slot_map, n_groups=E)
-print(json.dumps({"kernel": "gate", "us": ms * 1e3, "GBps": T * d * 2 / (ms * 1e-3) / 1e9,
+print(json.dumps({"kernel": "gate", "mode": mode, "min_us": min(ts) * 1e3, "us": ms * 1e3, "GBps": T * d * 2 / (ms * 1e-3) / 1e9,
                   "env": {k: v for k, v in os.environ.items() if k.startswith("COMOE_")}}))

@@ -58,8 +58,16 @@ def _check_routing(layer, x, wg, info, T):
     gp = g.gate_prob.cpu().numpy().astype(np.float64)
     assert np.max(np.abs(gp - info["prob"])) < PROB_TOL
     np.testing.assert_array_equal(g.local_rank.cpu().numpy(), info["local_rank"])
-    np.testing.assert_array_equal(g.tile_hist.cpu().numpy(), info["tile_hist"])
     s = r.scan
+    # stream-order tile prefixes (first choices in token order, then second
+    # choices): written by the gate's folded look-back, or by the scan kernel
+    # from the histograms (COMOE_GATE_FOLD=0)
+    hist = info["tile_hist"].reshape(-1, info["tile_hist"].shape[-1])
+    np.testing.assert_array_equal(s.tile_offset.cpu().numpy().reshape(hist.shape),
+                                  np.cumsum(hist, axis=0) - hist)
+    from paper_2508_09208_b200.layer import _gate_fold
+    if not _gate_fold():
+        np.testing.assert_array_equal(g.tile_hist.cpu().numpy(), info["tile_hist"])
     np.testing.assert_array_equal(s.group_count.cpu().numpy(), info["count"])
     np.testing.assert_array_equal(s.group_kept.cpu().numpy(), info["kept"])
     np.testing.assert_array_equal(s.group_base.cpu().numpy(), info["base"])
