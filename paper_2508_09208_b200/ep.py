@@ -25,6 +25,7 @@ forward over rank r's tokens.
 from __future__ import annotations
 
 import os
+from dataclasses import dataclass
 
 import torch
 import torch.distributed as dist
@@ -35,6 +36,60 @@ from .pool import ExpertPool
 
 def ep_capacity(tokens_per_rank: int, n_experts: int, top_k: int, capacity_factor) -> int:
     return kernels.capacity_for(tokens_per_rank, n_experts, top_k, capacity_factor)
+
+
+@dataclass
+class EPPlacement:
+    """Where the groups of a (possibly merged) variant live under expert
+    parallelism. A group is placed on the rank that owns its principal
+    expert under the block partition of the original experts (expert e on
+    rank e // (E / world)), so a merged expert is computed where its
+    principal already was. Groups are numbered in ascending principal order
+    (ModelVariant.group_table), so each rank's groups are consecutive.
+
+    Every rank gets the same number L of group slots (the most any rank
+    holds); group g is routed as padded index owner(g) * L + local(g). The
+    padded routing space has world * L <= E groups, some permanently
+    empty, which keeps every exchange block the same size (fixed-layout
+    all-to-all chunks, uniform peer blocks) while capacity stays
+    C = ceil(cf * T * k / G) over the variant's real G groups."""
+    E: int
+    world: int
+    G: int
+    L: int
+    owner: list          # [G] rank of each group
+    local: list          # [G] index among its rank's groups
+    slot_map: list       # [E] original expert -> padded group index
+    n_local: list        # [world] groups per rank
+
+    @property
+    def G_pad(self) -> int:
+        return self.world * self.L
+
+    def local_groups(self, rank: int) -> list:
+        """Group indices (variant numbering) of `rank`, in local order."""
+        return [g for g in range(self.G) if self.owner[g] == rank]
+
+
+def ep_placement(lut, principals, E: int, world: int) -> EPPlacement:
+    """lut[E] -> group index, principals[G] ascending (ModelVariant.group_table)."""
+    if E % world:
+        raise ValueError(f"{E} experts do not split over {world} ranks")
+    El = E // world
+    G = len(principals)
+    if list(principals) != sorted(principals) or len(set(principals)) != G:
+        raise ValueError("principals must be distinct and ascending")
+    if len(lut) != E or any(not 0 <= g < G for g in lut):
+        raise ValueError("lut must map every expert to a group")
+    owner = [int(p) // El for p in principals]
+    n_local = [owner.count(r) for r in range(world)]
+    L = max(n_local)
+    local, seen = [], [0] * world
+    for g in range(G):
+        local.append(seen[owner[g]])
+        seen[owner[g]] += 1
+    padded = [owner[g] * L + local[g] for g in range(G)]
+    return EPPlacement(E, world, G, L, owner, local, [padded[g] for g in lut], n_local)
 
 
 class _NoStage:
@@ -191,7 +246,7 @@ class DeviceOps:
 
     def dispatch(self, x, route, C):
         L = self.layer
-        dev, T, E, d = x.device, x.shape[0], L.E, L.d
+        dev, T, E, d = x.device, x.shape[0], L.G, L.d  # E: routing groups
         rows = E * C
         base = self._buf(("base", E, C),
                          lambda: torch.arange(E, dtype=torch.int32, device=dev) * C)
@@ -209,7 +264,7 @@ class DeviceOps:
         """Permute straight into the owners' receive buffers and scatter the
         per-expert row counts; returns token_pos (send-layout rows)."""
         L = self.layer
-        dev, T, E = x.device, x.shape[0], L.E
+        dev, T, E = x.device, x.shape[0], L.G  # E: routing groups
         rows = E * C
         if rows != bufs.rows:
             raise ValueError(f"peer buffers hold {bufs.rows} rows, this batch needs {rows}")
@@ -245,8 +300,10 @@ class DeviceOps:
             torch.arange(G, device=dev) % world * El + torch.arange(G, device=dev) // world
         ).to(torch.int64))
         base = self._buf(("gbase", world, El, C), lambda: (block * C).to(torch.int32))
-        slot = self._buf(("gslot", world, El),
-                         lambda: (torch.arange(G, dtype=torch.int32, device=dev) // world).contiguous())
+        local_slots = getattr(self, "local_slots", None)
+        slot = self._buf(("gslot", world, El), lambda: (
+            torch.arange(G, device=dev) // world if local_slots is None else
+            local_slots.to(dev)[torch.arange(G, device=dev) // world]).to(torch.int32).contiguous())
         recv_counts = recv_counts.index_select(0, block).contiguous()
         self.last_recv_counts = recv_counts  # rows this rank computes (bench FLOP count)
         rows = recv_rows.shape[0]
@@ -276,25 +333,44 @@ class DeviceOps:
 class EPMoELayer:
     """MoE layer with experts sharded over the ranks of `group`.
 
-    Holds the full router and this rank's E/world experts in an ExpertPool
-    (local slot le = global expert rank*E_l + le)."""
+    Holds the full router and this rank's groups in an ExpertPool. Without a
+    variant every expert is its own group and rank r holds experts
+    [r*E/world, (r+1)*E/world) in pool slots 0..E/world-1. With a merged
+    variant (`variant_table` = ModelVariant.group_table(layer, E)) each group
+    lives on its principal's rank (ep_placement) and `local_slots[i]` is the
+    pool slot of this rank's i-th group."""
 
     def __init__(self, wg, pool: ExpertPool, d_ff: int, world: int, rank: int, act="relu",
-                 top_k=1, norm_topk=None, capacity_factor=1.25, group=None, transport=None):
+                 top_k=1, norm_topk=None, capacity_factor=1.25, group=None, transport=None,
+                 variant_table=None, local_slots=None):
         from .layer import MoELayer
         d, E = wg.shape
         if E % world:
             raise ValueError(f"{E} experts do not split over {world} ranks")
-        if pool.n_slots < E // world:
-            raise ValueError("pool must hold this rank's E/world experts")
-        self.world, self.rank, self.E, self.El = world, rank, E, E // world
+        lut, principals = variant_table if variant_table is not None else \
+            (list(range(E)), list(range(E)))
+        self.placement = ep_placement(lut, principals, E, world)
+        n_mine = self.placement.n_local[rank]
+        if local_slots is None:
+            local_slots = list(range(n_mine))
+        if len(local_slots) != n_mine or any(not 0 <= s < pool.n_slots for s in local_slots):
+            raise ValueError(f"pool must hold this rank's {n_mine} groups (local_slots)")
+        self.world, self.rank, self.E = world, rank, E
+        self.G = self.placement.G
+        self.El = self.placement.L          # group slots per rank (padded)
+        self.G_pad = self.placement.G_pad   # routing groups (with empty placeholders)
         self.group = group
         self.capacity_factor = capacity_factor
-        # gate/scan run on all E experts; with G = E groups the per-rank
-        # capacity of MoELayer equals the EP capacity ceil(cf*T_g*k/E)
+        # gate/scan run over the padded group space; capacity uses the
+        # variant's real group count (== E without a variant)
         self.local = MoELayer(wg, pool, d_ff, act=act, top_k=top_k, norm_topk=norm_topk,
                               capacity_factor=capacity_factor, expert_slots=[0] * E)
+        self.local.set_variant(self.placement.slot_map, [0] * self.G_pad,
+                               capacity_groups=self.G)
         self.ops = DeviceOps(self.local)
+        self.ops.local_slots = torch.tensor(list(local_slots) + [local_slots[0] if local_slots
+                                                                  else 0] * (self.El - n_mine),
+                                            dtype=torch.int64)
         # "nccl": two ncclAllToAll per forward; "peer": stores / loads into the
         # peers' HBM over NVLink (CUDA IPC) with flag barriers
         self.transport = transport or os.environ.get("COMOE_EP_TRANSPORT", "nccl")
@@ -312,7 +388,7 @@ class EPMoELayer:
         return cls(wg, pool, d_ff, world, rank, act=act, capacity_factor=capacity_factor)
 
     def capacity(self, T: int) -> int:
-        return ep_capacity(T, self.E, self.local.top_k, self.capacity_factor)
+        return ep_capacity(T, self.G, self.local.top_k, self.capacity_factor)
 
     @property
     def last(self):
@@ -322,11 +398,11 @@ class EPMoELayer:
         """The peer-transport buffers for T tokens per rank (collective on
         first use and whenever the capacity changes: every rank calls it
         with the same T)."""
-        rows = self.E * self.capacity(T)
+        rows = self.G_pad * self.capacity(T)
         if self.peers is None or self.peers.rows != rows:
             if self.peers is not None:
                 self.peers.close()
-            self.peers = PeerBuffers(rows, self.local.d, self.E, self.world, self.rank,
+            self.peers = PeerBuffers(rows, self.local.d, self.G_pad, self.world, self.rank,
                                      self.local.wg.device, group=self.group)
         return self.peers
 
@@ -340,13 +416,13 @@ class EPMoELayer:
         C = self.capacity(x.shape[0])
         if self.transport == "peer":
             bufs = self.peer_buffers(x.shape[0])
-            y = ep_forward_peers(x, self.ops, bufs, self.E, C, stage=timer)
+            y = ep_forward_peers(x, self.ops, bufs, self.G_pad, C, stage=timer)
             self._calls = getattr(self, "_calls", 0) + 1
             if self._calls % self.err_check_every == 0 and \
                     not torch.cuda.is_current_stream_capturing():
                 bufs.check()
         else:
-            y = ep_forward(x, self.ops, self.world, self.E, C, group=self.group, stage=timer)
+            y = ep_forward(x, self.ops, self.world, self.G_pad, C, group=self.group, stage=timer)
         if out is not None:
             out.copy_(y)
             return out
@@ -356,5 +432,7 @@ class EPMoELayer:
 
     @property
     def kernels_per_forward(self) -> int:
-        # gate, scan, permute, 2x GEMM, combine (NCCL's all-to-all kernels not counted)
-        return 6
+        # gate (+ scan unless folded), permute, 2x GEMM, combine (NCCL's
+        # all-to-all kernels not counted)
+        from .layer import _gate_fold
+        return 5 if _gate_fold() else 6

@@ -97,9 +97,12 @@ class MoELayer:
         self.last: LayerRouting = None
 
     # ------------------------------------------------------------ variants
-    def set_variant(self, slot_map, group_slots) -> None:
+    def set_variant(self, slot_map, group_slots, capacity_groups: int = None) -> None:
         """slot_map[E]: original expert -> group index; group_slots[G]: pool
-        slot serving each group (ModelVariant.group_table gives both)."""
+        slot serving each group (ModelVariant.group_table gives both).
+        `capacity_groups`: the G of the capacity formula when the routing
+        groups include empty placeholders (expert parallelism pads every
+        rank to the same number of group slots; ep.ep_placement)."""
         slot_map = [int(s) for s in slot_map]
         group_slots = [int(s) for s in group_slots]
         G = len(group_slots)
@@ -109,6 +112,7 @@ class MoELayer:
             raise ValueError("group slot outside the pool")
         dev = self.wg.device
         self.G = G
+        self.capacity_groups = G if capacity_groups is None else int(capacity_groups)
         self.slot_map_host = list(slot_map)
         self.slot_map = torch.tensor(slot_map, dtype=torch.int32, device=dev)
         self.group_slot = torch.tensor(group_slots, dtype=torch.int32, device=dev)
@@ -128,7 +132,7 @@ class MoELayer:
 
     # ------------------------------------------------------------ workspace
     def capacity(self, T: int) -> int:
-        return kernels.capacity_for(T, self.G, self.top_k, self.capacity_factor)
+        return kernels.capacity_for(T, self.capacity_groups, self.top_k, self.capacity_factor)
 
     @property
     def fused(self) -> bool:

@@ -21,17 +21,23 @@ T_G, D, D_FF, E, CF = 300, 64, 128, 8, 1.0
 class OracleOps:
     """CPU double of ep.DeviceOps (test infrastructure)."""
 
-    def __init__(self, wg, w_in, w_out, rank, world, top_k=1):
+    def __init__(self, wg, w_in, w_out, rank, world, top_k=1, placement=None):
+        """placement: ep.EPPlacement of a merged variant (w_in / w_out are
+        then indexed by the variant's group); None = one group per expert."""
         self.wg, self.w_in, self.w_out = wg, w_in, w_out
         self.rank, self.world, self.top_k = rank, world, top_k
-        self.El = E // world
+        self.pl = placement
+        self.El = E // world if placement is None else placement.L
+        self.G_pad = E if placement is None else placement.G_pad
+        self.G = E if placement is None else placement.G
 
     def route(self, x):
         xn = x.numpy()
         logits = O.gate_logits(xn, self.wg)
-        idx, grp, prob = O.topk_route(logits, self.top_k, self.top_k == 2)
-        C = O.capacity(xn.shape[0], E, self.top_k, CF)
-        disp = O.dispatch_fast(grp, E, C)
+        sm = None if self.pl is None else self.pl.slot_map
+        idx, grp, prob = O.topk_route(logits, self.top_k, self.top_k == 2, sm)
+        C = O.capacity(xn.shape[0], self.G, self.top_k, CF)
+        disp = O.dispatch_fast(grp, self.G_pad, C)
 
         class R:
             pass
@@ -44,7 +50,7 @@ class OracleOps:
 
     def dispatch(self, x, route, C):
         xn = x.numpy()
-        rows = np.zeros((E * C, xn.shape[1]), np.float32)
+        rows = np.zeros((self.G_pad * C, xn.shape[1]), np.float32)
         pos = np.full(route.group.shape, -1, np.int64)
         for t in range(xn.shape[0]):
             for j in range(self.top_k):
@@ -63,7 +69,8 @@ class OracleOps:
                 n = int(cnt[g])
                 if n == 0:
                     continue
-                e = self.rank * El + le
+                e = self.rank * El + le if self.pl is None else \
+                    self.pl.local_groups(self.rank)[le]
                 xs = recv_rows[g * C:g * C + n].numpy().astype(np.float64)
                 y = O.expert_ffn(xs, self.w_in[e], self.w_out[e], "relu", round_h=False)
                 out[g * C:g * C + n] = torch.from_numpy(y.astype(np.float32))
@@ -97,6 +104,68 @@ def _worker(rank, world, port, q):
         q.put((rank, float(np.abs(y - ref).max()), int((info["pos"] < 0).sum())))
     finally:
         dist.destroy_process_group()
+
+
+# a merged 8 -> 4 variant whose principals are unevenly spread over 2 ranks
+# (rank 0 owns principals 0, 2, 3; rank 1 owns 5): L = 3 group slots per
+# rank, a padded routing space of 6 groups, capacity over the real 4
+MERGED_PRINCIPALS = [0, 2, 3, 5]
+MERGED_LUT = [0, 0, 1, 2, 1, 3, 3, 2]
+
+
+def _merged_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2508_09208_b200.ep import ep_forward, ep_placement
+        pl = ep_placement(MERGED_LUT, MERGED_PRINCIPALS, E, world)
+        rng = np.random.default_rng(1)
+        wg = (rng.normal(size=(D, E)) / 8).astype(np.float32)
+        G = len(MERGED_PRINCIPALS)
+        w_in = O.bf16_round(rng.normal(size=(G, D_FF, D)) * 0.05)
+        w_out = O.bf16_round(rng.normal(size=(G, D, D_FF)) * 0.05)
+        xs = [O.bf16_round(np.random.default_rng(20 + r).normal(size=(T_G, D))) for r in range(world)]
+        ops = OracleOps(wg, w_in, w_out, rank, world, placement=pl)
+        C = O.capacity(T_G, G, 1, CF)
+        y = ep_forward(torch.from_numpy(xs[rank]), ops, world, pl.G_pad, C).numpy()
+        ref, info = O.layer_forward_fast(xs[rank], wg, w_in, w_out, 1, False, CF,
+                                         slot_map=MERGED_LUT, dtype=np.float64)
+        q.put((rank, float(np.abs(y - ref).max()), int((info["pos"] < 0).sum())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ep_placement_tables():
+    from paper_2508_09208_b200.ep import ep_placement
+    pl = ep_placement(MERGED_LUT, MERGED_PRINCIPALS, E, 2)
+    assert pl.owner == [0, 0, 0, 1] and pl.local == [0, 1, 2, 0]
+    assert pl.n_local == [3, 1] and pl.L == 3 and pl.G_pad == 6
+    # padded index owner*L + local; every expert follows its group
+    assert pl.slot_map == [0, 0, 1, 2, 1, 3, 3, 2]
+    assert pl.local_groups(0) == [0, 1, 2] and pl.local_groups(1) == [3]
+    ident = ep_placement(list(range(E)), list(range(E)), E, 4)
+    assert ident.slot_map == list(range(E)) and ident.L == 2 and ident.G_pad == E
+    with pytest.raises(ValueError):
+        ep_placement(MERGED_LUT, [2, 0, 3, 5], E, 2)
+
+
+def test_ep_merged_variant_world2_gloo():
+    """A merged variant under EP: groups on their principal's rank, padded
+    routing space, capacity over the real groups; each rank's output equals
+    the single-device oracle forward of the merged layer on its tokens."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_merged_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, err, dropped in res:
+        assert err < 1e-5, (rank, err)
+        assert dropped > 0
 
 
 def _free_port():

@@ -38,7 +38,8 @@ def _world(world, T, d, d_ff, E, cf, seed=11):
 
 def _alltoall_emulation(layers, xs, world, E, C):
     """The NCCL schedule of ep_forward with each all_to_all_single done as a
-    block transposition of the same device buffers."""
+    block transposition of the same device buffers (E: routing groups, the
+    padded space of a merged variant included)."""
     El = E // world
     blk = El * C
     routes, sends, tps = [], [], []
@@ -128,3 +129,70 @@ def test_ep_layer_peer_transport_world1():
     y2 = L.forward(xs[0])   # second forward: epochs 3, 4 on the same pads
     torch.cuda.synchronize()
     assert torch.equal(y2, y) and L.peers.epoch == 4
+
+
+def _merged_world(world, T, d, d_ff, E, principals, lut, cf, seed=21):
+    """Per-rank EPMoELayers of a merged variant: group g's weights live in
+    the pool of its principal's rank (ep_placement)."""
+    from paper_2508_09208_b200 import ExpertPool, kernels
+    from paper_2508_09208_b200.ep import EPMoELayer, ep_placement
+    g = torch.Generator().manual_seed(seed)
+    wg = torch.randn(d, E, generator=g) / math.sqrt(d)
+    numel = kernels.expert_numel(d, d_ff, kernels.ACT_RELU)
+    G = len(principals)
+    w = (torch.randn(G, numel, generator=g) * 0.02).to(torch.bfloat16)
+    pl = ep_placement(lut, principals, E, world)
+    layers = []
+    for r in range(world):
+        mine = pl.local_groups(r)
+        pool = ExpertPool(max(1, len(mine)) + 1, numel)
+        slots = list(range(1, len(mine) + 1))          # slot 0 left unused on purpose
+        for s_, grp in zip(slots, mine):
+            pool.data[s_, :numel].copy_(w[grp].cuda())
+        layers.append(EPMoELayer(wg.cuda(), pool, d_ff, world=world, rank=r, capacity_factor=cf,
+                                 transport="peer", variant_table=(lut, principals),
+                                 local_slots=slots))
+    xs = [torch.randn(T, d, generator=g).to(torch.bfloat16).cuda() for _ in range(world)]
+    return layers, xs, wg, w, pl
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_merged_variant_ep_peer_and_alltoall(world):
+    """A CoMoE 16 -> 7 variant under EP: principals unevenly spread over the
+    ranks. Peer transport == the all-to-all schedule bit for bit, counts in
+    place, and every rank's output == the single-device oracle forward of
+    the merged layer over its tokens (capacity over the 7 real groups)."""
+    from paper_2508_09208_b200.ep import PeerBuffers
+    E, d, d_ff, T, cf = 16, 256, 512, 700, 1.0
+    principals = [0, 1, 2, 5, 9, 12, 13]
+    lut = [0, 1, 2, 2, 1, 3, 3, 0, 4, 4, 5, 4, 5, 6, 6, 3]
+    layers, xs, wg, w, pl = _merged_world(world, T, d, d_ff, E, principals, lut, cf)
+    Gp, L = pl.G_pad, pl.L
+    C = layers[0].capacity(T)
+    assert C == math.ceil(cf * T / len(principals))
+    ref = _alltoall_emulation(layers, xs, world, Gp, C)
+    bufs = PeerBuffers.simulated(world, Gp * C, d, Gp, torch.device("cuda"))
+    routes, tps = [], []
+    for r, Lr in enumerate(layers):
+        routes.append(Lr.ops.route(xs[r]))
+        tps.append(Lr.ops.dispatch_peers(xs[r], routes[-1], C, bufs[r]).clone())
+    for q, Lr in enumerate(layers):
+        Lr.ops.expert_ffn(bufs[q].recv, bufs[q].counts, L, C, world, y_out=bufs[q].y)
+    outs = [Lr.ops.combine_peers(tps[r], routes[r], bufs[r]) for r, Lr in enumerate(layers)]
+    torch.cuda.synchronize()
+    wi = np.stack([O.split_expert(w[g].float().numpy(), d, d_ff, "relu")[0] for g in range(len(principals))])
+    wo = np.stack([O.split_expert(w[g].float().numpy(), d, d_ff, "relu")[1] for g in range(len(principals))])
+    for r in range(world):
+        assert torch.equal(outs[r], ref[r]), f"rank {r}"
+        exp = torch.cat([routes[s].kept[r * L:(r + 1) * L] for s in range(world)])
+        assert torch.equal(bufs[r].counts, exp)
+        y_ref, info = O.layer_forward_fast(xs[r].float().cpu().numpy(), wg.numpy(), wi, wo, 1,
+                                           False, cf, slot_map=lut, dtype=np.float64,
+                                           round_h=True)
+        assert (info["pos"] < 0).any()        # capacity drops exercised
+        assert O.normwise_error(outs[r].float().cpu().numpy(), y_ref) < 5e-3
+    # and through the public forward (IPC transport) at world 1
+    if world == 1:
+        y = layers[0].forward(xs[0])
+        torch.cuda.synchronize()
+        assert torch.equal(y, ref[0])
