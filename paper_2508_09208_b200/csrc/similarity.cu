@@ -320,21 +320,27 @@ __global__ void __launch_bounds__(128) sim_gram_mma_kernel(const void* const* __
 // - Warp 1: four MMAs per block into a fresh TMEM accumulator (4 of them),
 //   so the tensor core's fp32 sums stay as short as the mma.sync path's
 //   (accumulating 256 d in TMEM drifted 4e-7 relative on the diagonal).
-// - Warps 2-9 (two per TMEM lane quadrant, 64 columns each): add the two
-//   blocks of a group with one RN fp32 add, convert once (fp32 -> fp64
-//   runs on the XU pipe, which bounded a per-block fold) and accumulate in
-//   fp64 registers. The bf16 x bf16 products are exact.
+// - Warps 2-9 (two per TMEM lane quadrant): add the two blocks of a group
+//   with one RN fp32 add and fold the sum into fp64 / compensated fp32
+//   register accumulators, one of each transposed pair of 32 x 32 tiles
+//   (see the fold below). The bf16 x bf16 products are exact.
 // Each CTA writes its fp64 [E,E] partial; sim_reduce_kernel sums them in a
 // fixed order. Every row is read once (the mma.sync tiles re-read each row
 // ~5x at E = 128).
-constexpr int kGtStages = 8;
+#ifndef COMOE_GT_STAGES
+#define COMOE_GT_STAGES 8
+#endif
+constexpr int kGtStages = COMOE_GT_STAGES;
 constexpr int kGtTile = 128 * 128;  // bytes per stage (128 rows x 64 bf16)
 constexpr int kGtSmem = 1024 + kGtStages * kGtTile + 256;
 constexpr int kGtThreads = 10 * 32;
 
 __global__ void __launch_bounds__(kGtThreads, 1)
     sim_gram_tc_kernel(const __grid_constant__ CUtensorMap tmap, int row0, int box_rows, int E,
-                       long n_kb, double* __restrict__ partial) {
+                       long n_kb, double* __restrict__ partial, int flags) {
+  // flags: 1 = contiguous block ranges per CTA; dev attribution (COMOE_GRAM_DEBUG,
+  // results invalid): 2 = the fold skips its arithmetic, 4 = no MMAs
+  const bool contig = flags & 1;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -345,7 +351,12 @@ __global__ void __launch_bounds__(kGtThreads, 1)
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n = static_cast<int>((n_kb - blockIdx.x + gridDim.x - 1) / gridDim.x);
+  // block i of this CTA: blockIdx.x + i * grid (interleaved) or, with
+  // `contig`, kb0 + i over a contiguous range of per = ceil(n_kb / grid)
+  const long per = (n_kb + gridDim.x - 1) / gridDim.x;
+  const long kb0 = static_cast<long>(blockIdx.x) * per;
+  const int n = contig ? static_cast<int>(kb0 < n_kb ? (n_kb - kb0 < per ? n_kb - kb0 : per) : 0)
+                       : static_cast<int>((n_kb - blockIdx.x + gridDim.x - 1) / gridDim.x);
 
   if (box_rows < 128)
     for (int i = threadIdx.x; i < kGtStages * kGtTile / 16; i += blockDim.x)
@@ -376,7 +387,8 @@ __global__ void __launch_bounds__(kGtThreads, 1)
         const int s = i % kGtStages;
         if (i >= kGtStages) mbar_wait(&empty_bar[s], ((i / kGtStages) - 1) & 1);
         mbar_expect_tx(&full_bar[s], static_cast<uint32_t>(box_rows) * 128u);
-        const int x = static_cast<int>((blockIdx.x + static_cast<long>(i) * gridDim.x) * 64);
+        const int x = static_cast<int>(
+            (contig ? kb0 + i : blockIdx.x + static_cast<long>(i) * gridDim.x) * 64);
         tma_load_2d(tiles + s * kGtTile, &tmap, &full_bar[s], x, row0);
       }
     }
@@ -394,50 +406,96 @@ __global__ void __launch_bounds__(kGtThreads, 1)
         const uint64_t desc = umma_desc_k_sw128(smem_u32(tiles + s * kGtTile));
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          umma_bf16(tmem_base + a * 128, desc + 2 * k, desc + 2 * k, kIdesc, k != 0 ? 1u : 0u);
+          if (!(flags & 4))
+            umma_bf16(tmem_base + a * 128, desc + 2 * k, desc + 2 * k, kIdesc, k != 0 ? 1u : 0u);
         umma_commit(&empty_bar[s]);
         if ((i & 1) == 1 || i == n - 1) umma_commit(&tfull_bar[pr]);
       }
     }
   } else {
     // ------------------------------------------------ fp64 fold (warps 2-9)
-    const int q = warp & 3, h = (warp - 2) >> 2;  // lane quadrant, column half
+    // Symmetric fold: of the 16 (row quadrant, 32-column block) tiles of the
+    // 128 x 128 accumulator only one of each transposed pair is folded —
+    // quadrant q takes column blocks q, q+1, q+2 (q < 2) or q, q+1 (q >= 2),
+    // mod 4: 10 tiles instead of 16, at most 3 per quadrant (the busiest
+    // scheduler's work drops a quarter and the accumulators fit in registers
+    // without spilling). Warp (q, h) takes half of its quadrant's 16-column
+    // chunks. Within a chunk the first 8 columns go fp32 -> fp64 (F2F on the
+    // XU pipe, which alone bounded the fold) + DADD and the other 8 stay in
+    // fp32 as an unevaluated sum hi + lo (Knuth two-sum on the FMA pipe, the
+    // rounding error of every add carried in lo: ~2^-44 relative, far inside
+    // the 1e-7 cosine bar), so the fold runs on two pipes at once.
+    const int q = warp & 3, h = (warp - 2) >> 2;  // lane quadrant, chunk half
     const int row = q * 32 + lane;
-    double acc[64];
+    constexpr int kMaxCh = 3;
+    const int nch = q < 2 ? 3 : 2;
+    const int ch0 = 2 * q + h * nch;  // global chunk of slot i: (ch0 + i) mod 8
+    double dacc[kMaxCh][8];
+    float fhi[kMaxCh][8], flo[kMaxCh][8];
 #pragma unroll
-    for (int c = 0; c < 64; ++c) acc[c] = 0.0;
+    for (int i = 0; i < kMaxCh; ++i)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        dacc[i][c] = 0.0;
+        fhi[i][c] = flo[i][c] = 0.f;
+      }
     const int n_groups = (n + 1) >> 1;
     for (int g = 0; g < n_groups; ++g) {
       const int pr = g & 1;
       const bool two = 2 * g + 1 < n;
       mbar_wait(&tfull_bar[pr], (g >> 1) & 1);
       tc_fence_after();
-      const uint32_t t = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + 2 * pr * 128 + h * 64;
+      const uint32_t t = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + 2 * pr * 128;
 #pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        uint32_t v[32], w[32];
-        tmem_ld32(t + half * 32, v);
-        tmem_ld32(t + 128 + half * 32, w);  // block 2g+1 (unused when absent)
+      for (int i = 0; i < kMaxCh; ++i) {
+        if (i >= nch) break;
+        const uint32_t col = static_cast<uint32_t>(((ch0 + i) & 7) * 16);
+        uint32_t v[16], w[16];
+        tmem_ld16(t + col, v);
+        tmem_ld16(t + 128 + col, w);  // block 2g+1 (unused when absent)
         tmem_ld_wait();
-        if (half == 1) {
+        if (i == nch - 1) {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty_bar[pr]);
         }
-        // one RN fp32 add of the two 64-d block sums, then one conversion:
-        // half the XU-pipe F2F work of folding every block
+        // one RN fp32 add of the two 64-d block sums, then the fold
+        if (flags & 2) continue;
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
+        for (int c = 0; c < 16; ++c) {
           const float x = __uint_as_float(v[c]) + (two ? __uint_as_float(w[c]) : 0.f);
-          acc[half * 32 + c] += static_cast<double>(x);
+          if (c < 8) {
+            dacc[i][c] += static_cast<double>(x);
+          } else {
+            const int k = c - 8;
+            const float sum = __fadd_rn(fhi[i][k], x);
+            const float bp = __fsub_rn(sum, fhi[i][k]);
+            const float err =
+                __fadd_rn(__fsub_rn(fhi[i][k], __fsub_rn(sum, bp)), __fsub_rn(x, bp));
+            fhi[i][k] = sum;
+            flo[i][k] = __fadd_rn(flo[i][k], err);
+          }
         }
       }
     }
-    if (row < E) {
-      double* out = partial + static_cast<long>(blockIdx.x) * E * E + static_cast<long>(row) * E;
+    // every (i, j) of the partial is written exactly once: diagonal tiles as
+    // folded, off-diagonal tiles at (row, col) and mirrored at (col, row)
+    double* out = partial + static_cast<long>(blockIdx.x) * E * E;
 #pragma unroll
-      for (int c = 0; c < 64; ++c)
-        if (h * 64 + c < E) out[h * 64 + c] = acc[c];
+    for (int i = 0; i < kMaxCh; ++i) {
+      if (i >= nch) break;
+      const int gc = (ch0 + i) & 7;
+      const bool diag = (gc >> 1) == q;
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        const int col = gc * 16 + c;
+        const double val = c < 8 ? dacc[i][c]
+                                 : static_cast<double>(fhi[i][c - 8]) + static_cast<double>(flo[i][c - 8]);
+        if (row < E && col < E) {
+          out[static_cast<long>(row) * E + col] = val;
+          if (!diag) out[static_cast<long>(col) * E + row] = val;
+        }
+      }
     }
   }
   tc_fence_before();
@@ -1189,8 +1247,13 @@ int comoe_sim_gram_strided(const void* base, long row_stride, int E, long D, dou
     attr = true;
   }
   double* partial = static_cast<double*>(work);
+  static const int contig = [] {
+    const char* e = std::getenv("COMOE_GRAM_CONTIG");
+    const char* d = std::getenv("COMOE_GRAM_DEBUG");
+    return (e && e[0] == '1' ? 1 : 0) | (d ? std::atoi(d) : 0);
+  }();
   sim_gram_tc_kernel<<<ctas, kGtThreads, kGtSmem, s>>>(tmap, 0, box_rows, E, (D + 63) / 64,
-                                                        partial);
+                                                        partial, contig);
   rc = check_launch("sim_gram_tc_kernel");
   if (rc) return rc;
   const long nn = static_cast<long>(E) * E;
