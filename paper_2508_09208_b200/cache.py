@@ -291,6 +291,24 @@ class ExpertCache:
                           bytes=b)
         return out
 
+    def room(self) -> int:
+        """Pool slots a wave of misses can use now: every slot not holding a
+        pinned resident expert (pinned = this wave's, hard-pinned, or an
+        in-flight prefetch)."""
+        held = sum(1 for e in self.slot_of if e in self.state.pinned)
+        return self.pool.n_slots - held
+
+    def drop_inflight_pins(self) -> None:
+        """Treat this step's in-flight prefetches as landed (the batched
+        stand-in for the simulator's arrival sweep): their pins only guard
+        the policy state, since a copy into a slot and any later reuse of
+        that slot are ordered on the copy stream. Used when a wave of
+        demand misses would otherwise find no slot."""
+        for e in sorted(self.inflight):
+            if e not in self.hard_pinned:
+                self.state.pinned.discard(e)
+        self.inflight.clear()
+
     def unpin(self, eids):
         for e in eids:
             if e not in self.hard_pinned and e not in self.inflight:
@@ -458,16 +476,32 @@ class CachedMoELayer:
         order = [int(g) for g in np.argsort(-kept, kind="stable") if kept[g] > 0]
         hits = [g for g in order if c.state.resident((lid, g))]
         misses = [g for g in order if not c.state.resident((lid, g))]
-        # every hit is already resident: one wave serves them all (no copies,
-        # no slots needed); only misses are bounded by the free slots
-        waves = ([hits] if hits else []) + \
-            [misses[i:i + self.wave_slots] for i in range(0, len(misses), self.wave_slots)]
         n1 = 2 * L.d_ff if L.act == "swiglu" else L.d_ff
         dst = out if k1 else ws["y_perm"]
         epi1 = kernels.EPI_SWIGLU if L.act == "swiglu" else kernels.EPI_RELU
         epi2 = kernels.EPI_SCALE_SCATTER if k1 else kernels.EPI_STORE
         tab = self._tables.numpy()
-        for w, wave in enumerate(waves):
+
+        def waves():
+            # every hit is already resident: one wave serves them all (no
+            # copies, no slots needed); a wave of misses takes at most
+            # wave_slots experts and never more than the slots free of pins
+            # right now (in-flight prefetches of this step hold theirs)
+            if hits:
+                yield hits
+            i = 0
+            while i < len(misses):
+                room = c.room()
+                if room < 1:
+                    c.drop_inflight_pins()
+                    room = c.room()
+                n = max(1, min(self.wave_slots, room))
+                yield misses[i:i + n]
+                i += n
+
+        for w, wave in enumerate(waves()):
+            if w >= self._tables.shape[0]:
+                raise InfeasibleError("more expert waves than groups")
             ids = [(lid, g) for g in wave]
             slots = c.serve(ids)
             c.stats.waves += 1

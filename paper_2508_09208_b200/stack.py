@@ -51,6 +51,69 @@ def fold_demand(demand, slot_map, n_groups: int, mode: str = "complement") -> np
     return 1.0 - miss
 
 
+class PrefetchGovernor:
+    """Turns predictive prefetch off when it does not pay (an extension of
+    the reference's threshold rule, which only gates individual experts).
+    Prefetches compete with demand fetches for the host link and evict
+    experts the batch would have hit, so whether they help depends on the
+    batch size and routing skew (scripts/bench_stack.py). The governor
+    measures it: per batch size it times `window` stack forwards with
+    prefetch on and `window` with it off (CUDA events on the compute
+    stream, read back without a sync one step later), keeps the faster
+    setting for `hold` steps, then probes again."""
+
+    def __init__(self, window: int = 3, hold: int = 24, margin: float = 0.0):
+        self.window, self.hold, self.margin = int(window), int(hold), float(margin)
+        self._st = {}
+        self._pending = None
+
+    def _state(self, T):
+        return self._st.setdefault(T, {"phase": "on", "left": self.window, "on": [], "off": [],
+                                       "choice": True})
+
+    def enabled(self, T: int) -> bool:
+        st = self._state(T)
+        return st["choice"] if st["phase"] == "hold" else st["phase"] == "on"
+
+    def begin(self, T: int):
+        self._collect()
+        start = torch.cuda.Event(enable_timing=True)
+        start.record()
+        return (T, self.enabled(T), start)
+
+    def end(self, token) -> None:
+        stop = torch.cuda.Event(enable_timing=True)
+        stop.record()
+        self._pending = (*token, stop)
+
+    def _collect(self) -> None:
+        if self._pending is None:
+            return
+        T, on, start, stop = self._pending
+        stop.synchronize()
+        self._pending = None
+        self.record(T, on, start.elapsed_time(stop))
+
+    def record(self, T: int, on: bool, ms: float) -> None:
+        """One measured stack forward of T tokens, prefetch `on` or off."""
+        st = self._state(T)
+        if st["phase"] == "hold":
+            st["left"] -= 1
+            if st["left"] <= 0:
+                st.update(phase="on", left=self.window, on=[], off=[])
+            return
+        st["on" if on else "off"].append(ms)
+        st["left"] -= 1
+        if st["left"] > 0:
+            return
+        if st["phase"] == "on":
+            st.update(phase="off", left=self.window)
+        else:
+            m_on, m_off = float(np.median(st["on"])), float(np.median(st["off"]))
+            st.update(phase="hold", left=self.hold, choice=m_on < m_off * (1.0 - self.margin),
+                      last=(m_on, m_off))
+
+
 @dataclass
 class StackLayer:
     index: int
@@ -71,9 +134,10 @@ class CachedMoEStack:
 
     def __init__(self, layers: list, predictor=None, policy: OffloadPolicy = None,
                  s_b: float = 1.0, mem_avail: float = 1.0, mem_total: float = 1.0,
-                 theta: float = None):
+                 theta: float = None, governor: PrefetchGovernor = None):
         self.layers = layers
         self.predictor = predictor
+        self.governor = governor
         self.policy = policy or OffloadPolicy()
         self.theta = prefetch_threshold(self.policy, s_b, mem_avail, mem_total) \
             if theta is None else float(theta)
@@ -100,11 +164,13 @@ class CachedMoEStack:
         self.steps = t + 1
         for c in self.caches():
             c.begin_step(t)
+        token = self.governor.begin(T) if self.governor is not None else None
+        predictive = self.predictor is not None and (token is None or token[1])
         h = x
         for i, sl in enumerate(self.layers):
             nxt = self.layers[i + 1] if i + 1 < len(self.layers) else None
             pre = post = None
-            if nxt is not None and sl.encoder and self.predictor is not None:
+            if nxt is not None and sl.encoder and predictive:
                 mode = "sum" if T == 1 else "any"
 
                 def pre(r, mode=mode):
@@ -129,4 +195,6 @@ class CachedMoEStack:
             y = sl.layer.forward(h, after_route=pre, after_serve=post, step=False,
                                  routing=routings[i] if routings is not None else None)
             h = (y.float() + h.float()).to(torch.bfloat16)
+        if token is not None:
+            self.governor.end(token)
         return h

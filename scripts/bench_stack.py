@@ -19,7 +19,7 @@ from paper_2508_09208_b200 import kernels
 from paper_2508_09208_b200.cache import CachedMoELayer, ExpertCache
 from paper_2508_09208_b200.moe import MoeModelSpec
 from paper_2508_09208_b200.offload import OffloadPolicy, train_predictor
-from paper_2508_09208_b200.stack import CachedMoEStack, StackLayer
+from paper_2508_09208_b200.stack import CachedMoEStack, PrefetchGovernor, StackLayer
 from paper_2508_09208_b200.traces import RoutingGeneratorSpec, generate_routing
 
 D, D_FF, E, SLOTS, LAYERS = 768, 3072, 128, 38, 4
@@ -42,14 +42,15 @@ def main():
         train = generate_routing(RoutingGeneratorSpec(skew=s, rho=0.9, seed=1), spec, 2048)
         mlp, metrics = train_predictor(train, hidden_dim=32, epochs=4)
         for T in (16, 64, 256, 1024):
-            n_batches = max(8, min(32, 8192 // T))
+            n_batches = max(48, min(96, 16384 // T))
             trace = generate_routing(RoutingGeneratorSpec(skew=s, rho=0.9, seed=2), spec,
                                      T * n_batches)
             idx = [torch.as_tensor(trace.expert_indices(l + 1)).cuda() for l in range(LAYERS)]
             emb = torch.as_tensor(np.stack([t.embedding for t in trace.tokens])).cuda()
             ctx = torch.as_tensor(np.stack([t.context for t in trace.tokens])).cuda()
             x = torch.randn(T, D, generator=g).to(torch.bfloat16).cuda()
-            for predictive in (False, True):
+            for mode in ("off", "on", "governed"):
+                predictive = mode != "off"
                 layers = []
                 for l in range(LAYERS):
                     cache = ExpertCache(hosts[l], layer=l + 1, n_slots=SLOTS, workspace_slots=2)
@@ -57,7 +58,8 @@ def main():
                                                                    capacity_factor=None)))
                 stack = CachedMoEStack(layers, predictor=mlp if predictive else None,
                                        policy=OffloadPolicy(), s_b=1.0, mem_avail=0.3,
-                                       mem_total=1.0)
+                                       mem_total=1.0,
+                                       governor=PrefetchGovernor() if mode == "governed" else None)
                 torch.cuda.synchronize()
                 t0 = time.perf_counter()
                 for b in range(n_batches):
@@ -69,7 +71,8 @@ def main():
                 st = [sl_.layer.cache.stats for sl_ in layers]
                 dem, hits = sum(x_.demand for x_ in st), sum(x_.hits for x_ in st)
                 out.append({"zipf_s": s, "tokens": T, "batches": n_batches,
-                            "predictor": predictive, "predictor_val_top1": metrics["val_top1"],
+                            "predictor": predictive, "mode": mode,
+                            "predictor_val_top1": metrics["val_top1"],
                             "hit_rate": hits / max(1, dem),
                             "demand_fetches": sum(x_.fetches for x_ in st),
                             "prefetch_issued": sum(x_.prefetch_issued for x_ in st),

@@ -190,3 +190,27 @@ def test_offload_priority_matches_reference():
                 offload_priority(*c["args"])
         else:
             assert offload_priority(*c["args"]) == c["value"]
+
+
+def test_prefetch_governor_keeps_the_faster_setting():
+    """PrefetchGovernor (stack.py): probe `window` forwards with prefetch on,
+    `window` off, hold the faster for `hold` steps, probe again; state is
+    kept per batch size."""
+    from paper_2508_09208_b200.stack import PrefetchGovernor
+    g = PrefetchGovernor(window=2, hold=3)
+    seq = []
+    for step in range(9):
+        on = g.enabled(64)
+        seq.append(on)
+        g.record(64, on, 10.0 if on else 7.0)   # prefetch costs time at 64 tokens
+    # on, on (probe), off, off (probe), off x3 (hold the faster), on, on (re-probe)
+    assert seq == [True, True, False, False, False, False, False, True, True]
+    assert g._state(64)["last"] == (10.0, 7.0)
+    g2 = PrefetchGovernor(window=1, hold=2)
+    seq = []
+    for step in range(4):
+        on = g2.enabled(16)
+        seq.append(on)
+        g2.record(16, on, 3.0 if on else 5.0)   # prefetch pays at 16 tokens
+    assert seq == [True, False, True, True]
+    assert g2.enabled(1024)  # a new batch size starts probing with prefetch on
