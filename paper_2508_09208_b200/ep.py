@@ -24,6 +24,7 @@ forward over rank r's tokens.
 
 from __future__ import annotations
 
+import functools
 import os
 from dataclasses import dataclass
 
@@ -100,27 +101,83 @@ class _NoStage:
         return False
 
 
-def ep_forward(x, ops, world: int, n_experts: int, capacity: int, group=None, stage=None):
+@functools.lru_cache(maxsize=64)
+def ep_chunk_base(n_groups: int, world: int, capacity: int, chunks: int, device="cpu"):
+    """Send-layout row base of every routing group for a `chunks`-way
+    exchange: group g = dst * El + le goes to block
+    ((le // Lc) * world + dst) * Lc + le % Lc (Lc = El / chunks), so chunk k
+    of the send buffer is one contiguous [dst][Lc][C] all-to-all. chunks = 1
+    is the plain [dst][El][C] layout (base = g * C)."""
+    El = n_groups // world
+    if El % chunks:
+        raise ValueError(f"{El} groups per rank do not split into {chunks} chunks")
+    Lc = El // chunks
+    g = torch.arange(n_groups)
+    dst, le = g // El, g % El
+    return ((((le // Lc) * world + dst) * Lc + le % Lc) * capacity).to(torch.int32).to(device)
+
+
+def ep_forward(x, ops, world: int, n_experts: int, capacity: int, group=None, stage=None,
+               chunks: int = 1):
     """One EP layer forward of this rank's tokens `x` [T_g, d]. `stage`:
-    optional callable(name) -> context manager timing each step (bench.py)."""
+    optional callable(name) -> context manager timing each step (bench.py).
+
+    chunks > 1 pipelines the exchange over groups of local experts: the send
+    buffer is laid out [chunk][dst][El/chunks][C] (ep_chunk_base), every
+    chunk's dispatch all-to-all is issued asynchronously up front, and chunk
+    k's grouped FFN runs as soon as its rows have arrived — while chunk
+    k+1's rows are still in flight — and its outputs go back asynchronously
+    while chunk k+1 computes. Each expert's weights are still read once per
+    chunk it belongs to, i.e. once."""
     st = stage if stage is not None else (lambda name: _NoStage())
     E, C = n_experts, capacity
     El = E // world
     with st("route"):
         route = ops.route(x)                                # gate + scan (counts per global expert)
+    if chunks == 1:
+        with st("permute"):
+            send_rows, token_pos = ops.dispatch(x, route, C)    # [E*C, d] fixed layout
+        kept = route.kept                                       # [E] int32, rows per expert from me
+        with st("a2a_dispatch"):
+            recv_counts = torch.empty_like(kept)
+            dist.all_to_all_single(recv_counts, kept, group=group)
+            recv_rows = torch.empty_like(send_rows)
+            dist.all_to_all_single(recv_rows, send_rows, group=group)
+        # groups on the receiver: (src, local expert) -> rows recv_counts[src*El+le]
+        y_recv = ops.expert_ffn(recv_rows, recv_counts, El, C, world, stage=st)
+        with st("a2a_combine"):
+            y_back = torch.empty_like(y_recv)
+            dist.all_to_all_single(y_back, y_recv, group=group)
+        with st("combine"):
+            return ops.combine(y_back, token_pos, route)
+    Lc = El // chunks
+    base = ep_chunk_base(E, world, C, chunks, x.device)
     with st("permute"):
-        send_rows, token_pos = ops.dispatch(x, route, C)    # [E*C, d] fixed layout
-    kept = route.kept                                       # [E] int32, rows per expert from me
+        send_rows, token_pos = ops.dispatch(x, route, C, base=base)
+    kept = route.kept
+    blk = world * Lc * C                                    # rows per chunk
     with st("a2a_dispatch"):
         recv_counts = torch.empty_like(kept)
         dist.all_to_all_single(recv_counts, kept, group=group)
         recv_rows = torch.empty_like(send_rows)
-        dist.all_to_all_single(recv_rows, send_rows, group=group)
-    # groups on the receiver: (src, local expert) -> rows recv_counts[src*El+le]
-    y_recv = ops.expert_ffn(recv_rows, recv_counts, El, C, world, stage=st)
+        sends = [dist.all_to_all_single(recv_rows[k * blk:(k + 1) * blk],
+                                        send_rows[k * blk:(k + 1) * blk], group=group,
+                                        async_op=True) for k in range(chunks)]
+    counts = recv_counts.view(world, chunks, Lc)           # [src][chunk][Lc]
+    y_recv = torch.empty_like(recv_rows)
+    y_back = torch.empty_like(recv_rows)
+    backs = []
+    for k in range(chunks):
+        sends[k].wait()
+        ops.expert_ffn(recv_rows[k * blk:(k + 1) * blk], counts[:, k].reshape(-1).contiguous(),
+                       Lc, C, world, stage=st, y_out=y_recv[k * blk:(k + 1) * blk],
+                       slot_offset=k * Lc)
+        backs.append(dist.all_to_all_single(y_back[k * blk:(k + 1) * blk],
+                                            y_recv[k * blk:(k + 1) * blk], group=group,
+                                            async_op=True))
     with st("a2a_combine"):
-        y_back = torch.empty_like(y_recv)
-        dist.all_to_all_single(y_back, y_recv, group=group)
+        for w in backs:
+            w.wait()
     with st("combine"):
         return ops.combine(y_back, token_pos, route)
 
@@ -244,12 +301,16 @@ class DeviceOps:
         self.layer.last = r
         return r
 
-    def dispatch(self, x, route, C):
+    def dispatch(self, x, route, C, base=None):
+        """Permute into the send buffer; `base` [E] (ep_chunk_base) gives each
+        group's first row (default g * C)."""
         L = self.layer
         dev, T, E, d = x.device, x.shape[0], L.G, L.d  # E: routing groups
         rows = E * C
-        base = self._buf(("base", E, C),
-                         lambda: torch.arange(E, dtype=torch.int32, device=dev) * C)
+        if base is None:
+            base = self._buf(("base", E, C),
+                             lambda: torch.arange(E, dtype=torch.int32, device=dev) * C)
+
         perm = self._buf(("perm", T, rows), lambda: kernels.PermuteOutput(
             torch.zeros((rows, d), dtype=torch.bfloat16, device=dev),
             torch.empty(rows, dtype=torch.int32, device=dev),
@@ -285,7 +346,8 @@ class DeviceOps:
         return kernels.combine_peers(bufs.y_ptrs, bufs.block_rows, bufs.rank, token_pos,
                                      route.gate.gate_prob, bufs.d)
 
-    def expert_ffn(self, recv_rows, recv_counts, El, C, world, stage=None, y_out=None):
+    def expert_ffn(self, recv_rows, recv_counts, El, C, world, stage=None, y_out=None,
+                   slot_offset: int = 0):
         """Grouped FFN over the receive buffer [src][local expert][C] rows.
         Groups are enumerated expert-major (j -> local expert j // world,
         source j % world), so the tiles of one expert's `world` source
@@ -301,11 +363,14 @@ class DeviceOps:
         ).to(torch.int64))
         base = self._buf(("gbase", world, El, C), lambda: (block * C).to(torch.int32))
         local_slots = getattr(self, "local_slots", None)
-        slot = self._buf(("gslot", world, El), lambda: (
-            torch.arange(G, device=dev) // world if local_slots is None else
-            local_slots.to(dev)[torch.arange(G, device=dev) // world]).to(torch.int32).contiguous())
+        slot = self._buf(("gslot", world, El, slot_offset), lambda: (
+            torch.arange(G, device=dev) // world + slot_offset if local_slots is None else
+            local_slots.to(dev)[torch.arange(G, device=dev) // world + slot_offset]
+        ).to(torch.int32).contiguous())
         recv_counts = recv_counts.index_select(0, block).contiguous()
-        self.last_recv_counts = recv_counts  # rows this rank computes (bench FLOP count)
+        # rows this rank computes (bench FLOP count; summed over the chunks)
+        self.last_recv_counts = recv_counts if slot_offset == 0 else \
+            torch.cat([self.last_recv_counts, recv_counts])
         rows = recv_rows.shape[0]
         y = y_out if y_out is not None else self._buf(("y", rows),
                                                        lambda: torch.empty_like(recv_rows))
@@ -342,7 +407,7 @@ class EPMoELayer:
 
     def __init__(self, wg, pool: ExpertPool, d_ff: int, world: int, rank: int, act="relu",
                  top_k=1, norm_topk=None, capacity_factor=1.25, group=None, transport=None,
-                 variant_table=None, local_slots=None):
+                 variant_table=None, local_slots=None, chunks: int = None):
         from .layer import MoELayer
         d, E = wg.shape
         if E % world:
@@ -374,6 +439,14 @@ class EPMoELayer:
         # "nccl": two ncclAllToAll per forward; "peer": stores / loads into the
         # peers' HBM over NVLink (CUDA IPC) with flag barriers
         self.transport = transport or os.environ.get("COMOE_EP_TRANSPORT", "nccl")
+        # NCCL transport: the exchange pipelined over `chunks` groups of local
+        # experts (ep_forward); default 2 when there are peers to overlap with
+        if chunks is None:
+            env = os.environ.get("COMOE_EP_CHUNKS")
+            chunks = int(env) if env else (2 if world > 1 and self.El % 2 == 0 else 1)
+        if chunks < 1 or self.El % chunks:
+            raise ValueError(f"chunks={chunks} must divide the {self.El} group slots per rank")
+        self.chunks = chunks
         if self.transport not in ("nccl", "peer"):
             raise ValueError(f"unknown EP transport {self.transport!r}")
         self.peers = None
@@ -422,7 +495,8 @@ class EPMoELayer:
                     not torch.cuda.is_current_stream_capturing():
                 bufs.check()
         else:
-            y = ep_forward(x, self.ops, self.world, self.G_pad, C, group=self.group, stage=timer)
+            y = ep_forward(x, self.ops, self.world, self.G_pad, C, group=self.group, stage=timer,
+                           chunks=self.chunks)
         if out is not None:
             out.copy_(y)
             return out

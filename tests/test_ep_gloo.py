@@ -48,20 +48,22 @@ class OracleOps:
         r.kept = torch.tensor(disp["kept"], dtype=torch.int32)
         return r
 
-    def dispatch(self, x, route, C):
+    def dispatch(self, x, route, C, base=None):
         xn = x.numpy()
+        base = np.arange(self.G_pad) * C if base is None else base.numpy()
         rows = np.zeros((self.G_pad * C, xn.shape[1]), np.float32)
         pos = np.full(route.group.shape, -1, np.int64)
         for t in range(xn.shape[0]):
             for j in range(self.top_k):
                 g, rk = route.group[t, j], route.rank_[t, j]
                 if g >= 0 and rk < C:
-                    pos[t, j] = g * C + rk
+                    pos[t, j] = base[g] + rk
                     rows[pos[t, j]] = xn[t]
         return torch.from_numpy(rows), pos
 
-    def expert_ffn(self, recv_rows, recv_counts, El, C, world, stage=None):
-        out = torch.zeros_like(recv_rows)
+    def expert_ffn(self, recv_rows, recv_counts, El, C, world, stage=None, y_out=None,
+                   slot_offset=0):
+        out = torch.zeros_like(recv_rows) if y_out is None else y_out.zero_()
         cnt = recv_counts.numpy()
         for src in range(world):
             for le in range(El):
@@ -69,8 +71,11 @@ class OracleOps:
                 n = int(cnt[g])
                 if n == 0:
                     continue
-                e = self.rank * El + le if self.pl is None else \
-                    self.pl.local_groups(self.rank)[le]
+                lg = slot_offset + le                    # local group slot
+                e = self.rank * self.El + lg if self.pl is None else \
+                    self.pl.local_groups(self.rank)[lg]
+                if self.pl is not None and lg >= self.pl.n_local[self.rank]:
+                    continue
                 xs = recv_rows[g * C:g * C + n].numpy().astype(np.float64)
                 y = O.expert_ffn(xs, self.w_in[e], self.w_out[e], "relu", round_h=False)
                 out[g * C:g * C + n] = torch.from_numpy(y.astype(np.float32))
@@ -133,6 +138,56 @@ def _merged_worker(rank, world, port, q):
         q.put((rank, float(np.abs(y - ref).max()), int((info["pos"] < 0).sum())))
     finally:
         dist.destroy_process_group()
+
+
+def _chunked_worker(rank, world, port, chunks, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2508_09208_b200.ep import ep_forward
+        rng = np.random.default_rng(0)
+        wg = (rng.normal(size=(D, E)) / 8).astype(np.float32)
+        w_in = O.bf16_round(rng.normal(size=(E, D_FF, D)) * 0.05)
+        w_out = O.bf16_round(rng.normal(size=(E, D, D_FF)) * 0.05)
+        xs = [O.bf16_round(np.random.default_rng(10 + r).normal(size=(T_G, D))) for r in range(world)]
+        ops = OracleOps(wg, w_in, w_out, rank, world)
+        C = O.capacity(T_G, E, 1, CF)
+        y = ep_forward(torch.from_numpy(xs[rank]), ops, world, E, C, chunks=chunks).numpy()
+        ref, info = O.layer_forward_fast(xs[rank], wg, w_in, w_out, 1, False, CF,
+                                         dtype=np.float64)
+        q.put((rank, float(np.abs(y - ref).max()), int((info["pos"] < 0).sum())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ep_chunk_base_layout():
+    from paper_2508_09208_b200.ep import ep_chunk_base
+    # 8 groups, 2 ranks (El = 4), 2 chunks (Lc = 2), C = 10: send layout
+    # [chunk][dst][Lc][C]: chunk 0 = (d0: g0 g1 | d1: g4 g5), chunk 1 = (d0: g2 g3 | d1: g6 g7)
+    assert ep_chunk_base(8, 2, 10, 2).tolist() == [0, 10, 40, 50, 20, 30, 60, 70]
+    assert ep_chunk_base(8, 2, 10, 1).tolist() == [10 * g for g in range(8)]
+    with pytest.raises(ValueError):
+        ep_chunk_base(8, 2, 10, 3)
+
+
+@pytest.mark.parametrize("chunks", [2, 4])
+def test_ep_forward_chunked_world2_gloo(chunks):
+    """The chunked exchange (async all-to-all per chunk of local experts,
+    FFN of chunk k while chunk k+1 is in flight) gives every rank the same
+    output as the single-device oracle forward of its tokens."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_chunked_worker, args=(r, 2, port, chunks, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, err, dropped in res:
+        assert err < 1e-5, (rank, err)
+        assert dropped > 0
 
 
 def test_ep_placement_tables():

@@ -57,6 +57,13 @@ def test_expert_parallel_world1_matches_oracle():
     pool.data[:, :numel].copy_(w.cuda())
     layer = EPMoELayer(wg, pool, d_ff, world=1, rank=0, capacity_factor=1.0)
     y = layer.forward(x.cuda())
+    # the chunked exchange (async all-to-all per chunk of local experts,
+    # FFN of chunk k while chunk k+1 is in flight) computes every row the same
+    for chunks in (2, 4):
+        layer_c = EPMoELayer(wg, pool, d_ff, world=1, rank=0, capacity_factor=1.0, chunks=chunks)
+        yc = layer_c.forward(x.cuda())
+        torch.cuda.synchronize()
+        assert torch.equal(yc, y), chunks
     torch.cuda.synchronize()
     logits = None
     wi = np.stack([O.split_expert(w[e].float().numpy(), d, d_ff, "relu")[0] for e in range(E)])
