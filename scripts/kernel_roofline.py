@@ -89,12 +89,20 @@ def main():
     ms = timed(lambda: kernels.gate_topk(x, layer.wg_split, E, 1, False, slot_map=layer.slot_map,
                                          n_groups=E, out=ws["gate"]))
     line("gate_kernel (K1)", ms, gbytes, "T*d*2 (x) + Wg split + T*16 (idx,group,prob,rank) + hist",
-         flops=3 * 2 * T * d * 128)
+         flops=2 * 2 * T * d * 128)  # two bf16 split terms (gate_terms())
 
     # route scan: hist read + offsets written + [G] outputs
     sbytes = 2 * nt * E * 4 + 3 * E * 4
     ms = timed(lambda: kernels.route_scan(ws["gate"].tile_hist, ws["C"], out=ws["scan"]))
     line("route_scan", ms, sbytes, "tile_hist read + tile_offset write + 3*G")
+
+    # the production router: gate + capacity scan in one launch (comoe_gate_route)
+    lbw = kernels.gate_route_workspace(T, 1, E, dev)
+    ms = timed(lambda: kernels.gate_route(x, layer.wg_split, E, 1, False, ws["C"], lbw,
+                                          slot_map=layer.slot_map, n_groups=E, out=ws["gate"],
+                                          scan=ws["scan"]))
+    line("gate_route (K1 + folded scan)", ms, gbytes + sbytes,
+         "gate bytes + histogram write/read + tile_offset write + 3*G", flops=2 * 2 * T * d * 128)
 
     # K2 permute (top-1: copies kept rows, zeroes y rows of dropped tokens)
     pbytes = T * d * 2 + kept * d * 2 + (T - kept) * d * 2 + T * 4 * 4 + kept * 8
