@@ -203,6 +203,8 @@ def similarity_matrix(experts: list, alpha_sim: float, calib: Calibration) -> np
     if not (0.0 <= alpha_sim <= 1.0):
         raise ValueError(f"alpha_sim must be in [0, 1], got {alpha_sim}")
     rows = _rows(experts)
+    if not hasattr(calib, "device"):  # the reference's own Calibration (drop-in use)
+        calib = Calibration(probes=calib.probes, projection=calib.projection)
     probes, proj = calib.device(rows[0].device)
     sim, gram, _ = kernels.similarity(rows, probes, proj, alpha_sim)
     if torch.any(torch.diagonal(gram) == 0):
