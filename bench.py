@@ -413,7 +413,10 @@ def run_ours(args):
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    stages = {k: sum(a.elapsed_time(b) for a, b in v) / len(v) for k, v in stage_ev.items()}
+    # per-step stage time: summed over a step's launches of that stage (the
+    # chunked EP exchange runs each GEMM once per chunk, back to back on this
+    # stream), averaged over the timed steps
+    stages = {k: sum(a.elapsed_time(b) for a, b in v) / args.steps for k, v in stage_ev.items()}
 
     # tokens processed: every token passes the gate and the combine; report kept ratio too
     kept = int(layer.last.scan.group_kept.sum().item()) if hasattr(layer, "last") and layer.last else None
@@ -432,7 +435,10 @@ def run_ours(args):
                 "peak": bf16_peak, "unit": "TFLOP/s",
                 "frac": achieved / bf16_peak if achieved is not None else None,
                 "peak_source": peak_src,
-                "algorithmic": f"2*kept_rows*d*d_ff = {flops:.4g} FLOP per launch (kept_rows={rows})",
+                "algorithmic": f"2*kept_rows*d*d_ff = {flops:.4g} FLOP per launch (kept_rows={rows})"
+                               + (f"; {len(stage_ev[dom]) // args.steps} launches per step (EP chunks), "
+                                  "achieved over their summed time" if dom in stage_ev and
+                                  len(stage_ev[dom]) > args.steps else ""),
                 "traffic": prof.get(f"{dom}_dram_bytes_per_launch")}
     sustained = peaks.get("bf16_tflops_sustained")
     if sustained and achieved is not None:
