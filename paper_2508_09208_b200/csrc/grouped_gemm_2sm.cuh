@@ -370,6 +370,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k
           for (int j = 0; j < 32; ++j)
             v[j] = __float_as_uint(__uint_as_float(v[j]) * __shfl_sync(0xffffffffu, my_p, j));
         }
+        if (p.debug & 1024) continue;  // dev: epilogue math only (no staging, no stores)
         // register transpose of feature pairs: lanes (2p, 2p+1) hold features
         // (2p, 2p+1); for each token pair (2j, 2j+1) the even lane keeps token
         // 2j and the odd lane token 2j+1, one shfl_xor swapping the partner
@@ -400,9 +401,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k
           if (c + 32 <= t.ntok && !(p.debug & 4)) {
             fence_async_smem();
             __syncwarp();
-            if (lane == 0) {
+            if (lane == 0 && !(p.debug & 512)) {  // (dev 512: staged, not stored)
               tma_store_2d(&tmap_out, stg + (sg - smem_u32(stg)), static_cast<int>(col0),
-                           static_cast<int>(row_base + c));
+                           (p.debug & 2048) ? 0 : static_cast<int>(row_base + c));
               bulk_commit();
             }
             nbuf ^= 1;
@@ -415,10 +416,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k
             const int r = 8 * i + (lane >> 2), j = lane & 3;
             const uint4 x = lds128(sg + r * 64 + ((j ^ ((r >> 1) & 3)) << 4));
             const int tk = c + r;
-            if (tk < t.ntok) {
+            if (tk < t.ntok && !(p.debug & 512)) {
               long dst;
               if constexpr (kMode == kEpiScaleScatter) dst = __ldg(p.row_token + row_base + tk);
               else dst = row_base + tk;
+              if (p.debug & 2048) dst = r;  // dev: every tile writes the same 32 rows (L2-resident)
               st_global_v4(p.out + dst * p.ldo + col0 + j * 8, x.x, x.y, x.z, x.w);
             }
           }

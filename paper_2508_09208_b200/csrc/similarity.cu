@@ -339,7 +339,8 @@ __global__ void __launch_bounds__(kGtThreads, 1)
     sim_gram_tc_kernel(const __grid_constant__ CUtensorMap tmap, int row0, int box_rows, int E,
                        long n_kb, double* __restrict__ partial, int flags) {
   // flags: 1 = contiguous block ranges per CTA; dev attribution (COMOE_GRAM_DEBUG,
-  // results invalid): 2 = the fold skips its arithmetic, 4 = no MMAs
+  // results invalid): 2 = the fold skips its arithmetic, 4 = no MMAs, 8 = the
+  // MMA warp does not wait for the fold (the fold warps idle)
   const bool contig = flags & 1;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -400,7 +401,7 @@ __global__ void __launch_bounds__(kGtThreads, 1)
         // block i -> its own accumulator i % 4; blocks 2g, 2g+1 form fold
         // group g, handed over through the pair's barriers (g % 2)
         const int s = i % kGtStages, a = i & 3, g = i >> 1, pr = g & 1;
-        if ((i & 1) == 0) mbar_wait(&tempty_bar[pr], ((g >> 1) & 1) ^ 1);
+        if ((i & 1) == 0 && !(flags & 8)) mbar_wait(&tempty_bar[pr], ((g >> 1) & 1) ^ 1);
         mbar_wait(&full_bar[s], (i / kGtStages) & 1);
         tc_fence_after();
         const uint64_t desc = umma_desc_k_sw128(smem_u32(tiles + s * kGtTile));
@@ -409,7 +410,7 @@ __global__ void __launch_bounds__(kGtThreads, 1)
           if (!(flags & 4))
             umma_bf16(tmem_base + a * 128, desc + 2 * k, desc + 2 * k, kIdesc, k != 0 ? 1u : 0u);
         umma_commit(&empty_bar[s]);
-        if ((i & 1) == 1 || i == n - 1) umma_commit(&tfull_bar[pr]);
+        if (((i & 1) == 1 || i == n - 1) && !(flags & 8)) umma_commit(&tfull_bar[pr]);
       }
     }
   } else {
@@ -427,6 +428,8 @@ __global__ void __launch_bounds__(kGtThreads, 1)
     // the 1e-7 cosine bar), so the fold runs on two pipes at once.
     const int q = warp & 3, h = (warp - 2) >> 2;  // lane quadrant, chunk half
     const int row = q * 32 + lane;
+    if (flags & 8) goto fold_done;
+    {
     constexpr int kMaxCh = 3;
     const int nch = q < 2 ? 3 : 2;
     const int ch0 = 2 * q + h * nch;  // global chunk of slot i: (ch0 + i) mod 8
@@ -497,6 +500,8 @@ __global__ void __launch_bounds__(kGtThreads, 1)
         }
       }
     }
+    }
+  fold_done:;
   }
   tc_fence_before();
   __syncthreads();
