@@ -272,6 +272,14 @@ int comoe_predictor_mlp(const int* slots, int B, int K, const double* emb, int e
 /* dev: {clock64, ns} at the start and end of CTA 0 of the last 2-SM grouped
  * GEMM launched with COMOE_GEMM_DEBUG bit 256 — the SM clock under load */
 int comoe_debug_gemm_clock(unsigned long long* out4);
+/* dev: gate timeline of CTAs 0 and 1 ([2][1024] = [cta][code * 32 + unit
+ * iteration] of 1 + cycles since entry, 0 = not reached; COMOE_GATE_DEBUG bit
+ * 256), counts [2] = entries per CTA; resets them */
+int comoe_debug_gate_timeline(unsigned long long* out, unsigned int* counts);
+/* dev: router-in-TMEM gate variant for later launches (1 on, 0 off, -1: COMOE_GATE_TM) */
+int comoe_debug_set_gate_tm(int on);
+/* dev: override COMOE_GEMM_DEBUG for later grouped-GEMM launches (-1: env value) */
+int comoe_debug_set_gemm(int debug);
 
 #ifdef __cplusplus
 }

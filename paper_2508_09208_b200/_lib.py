@@ -47,6 +47,9 @@ _SIGNATURES = {
     "comoe_debug_fused_prof": [_p],
     "comoe_combine": [_p, _p, _p, _c_int, _c_int, _c_int, _p, _p],
     "comoe_debug_gemm_clock": [_p],
+    "comoe_debug_set_gemm": [_c_int],
+    "comoe_debug_gate_timeline": [_p, _p],
+    "comoe_debug_set_gate_tm": [_c_int],
     "comoe_permute_peers": [_p, _c_int, _c_int, _c_int, _p, _p, _p, _p, _p, _c_int, _c_int, _p,
                             _c_int, _c_long, _c_int, _p, _p, _p, _p],
     "comoe_combine_peers": [_p, _c_int, _c_long, _c_int, _p, _p, _c_int, _c_int, _c_int, _p, _p],

@@ -209,12 +209,15 @@ static int launch_gemm_2sm_small(const CUtensorMap& tw, const CUtensorMap& tx,
   return launch_gemm_2sm_cfg<kMode, 10, 4, 32>(tw, tx, to, p, stream);
 }
 
+// dev switches (COMOE_GEMM_DEBUG, or comoe_debug_set_gemm at run time so
+// A/B probes can alternate modes inside one process)
+static int g_gemm_debug_override = -1;
 static int gemm_debug() {
   static const int d = [] {
     const char* e = std::getenv("COMOE_GEMM_DEBUG");
     return e ? std::atoi(e) : 0;
   }();
-  return d;
+  return g_gemm_debug_override >= 0 ? g_gemm_debug_override : d;
 }
 
 // Tile order (both kernels): feature-tile major when one group's weight block
@@ -391,6 +394,12 @@ int comoe_debug_gemm_clock(unsigned long long* out4) {
   const cudaError_t e = cudaMemcpyFromSymbol(out4, g_gemm_clock, sizeof(unsigned long long) * 4);
   COMOE_REQUIRE(e == cudaSuccess, kCudaError, "debug_gemm_clock: %s", cudaGetErrorString(e));
   return kOk;
+}
+
+// dev: override COMOE_GEMM_DEBUG for later launches (-1 restores the env value)
+int comoe_debug_set_gemm(int debug) {
+  comoe::g_gemm_debug_override = debug;
+  return comoe::kOk;
 }
 
 }  // extern "C"

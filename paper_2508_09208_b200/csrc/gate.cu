@@ -100,6 +100,21 @@ __device__ __forceinline__ void red_release_gpu_add(unsigned int* a, unsigned in
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
 }
 
+// dev timeline (COMOE_GATE_DEBUG bit 256): CTAs 0 and 1 (one pair) stamp
+// clock64 - entry at slot [code][unit iteration] (plain stores, no atomics,
+// so the stamps do not delay the warps they time); comoe_debug_gate_timeline
+// copies them out
+constexpr int kGateTlMax = 1024;
+constexpr int kGateTlIters = 32;
+static __device__ unsigned long long g_gate_tl[2][kGateTlMax];
+__device__ __forceinline__ void gate_tl(const GateParams& p, long long t0, int code, int u) {
+  if (!(p.debug & 256) || blockIdx.x > 1) return;
+  // codes 1, 10-12 carry a raw value (warp); the rest a unit -> its iteration
+  const int iter = (code == 1 || (code >= 10 && code <= 12)) ? u : u / static_cast<int>(gridDim.x >> 1);
+  if (iter >= kGateTlIters) return;
+  g_gate_tl[blockIdx.x][code * kGateTlIters + iter] = static_cast<unsigned long long>(clock64() - t0) + 1ull;
+}
+
 constexpr int kFoldPer = 4;  // histogram entries per thread loaded before the scan
 
 // After the main loop (all kGateThreads threads of every CTA): grid barrier,
@@ -303,6 +318,7 @@ __global__ void __launch_bounds__(kGateThreads, 1)
   // left one full epilogue after the last MMA).
   constexpr bool kSplitEpi = kCat && EP >= 32;
   if (p.debug & 32) return;  // dev: empty launch
+  const long long tl0 = clock64();
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -364,6 +380,7 @@ __global__ void __launch_bounds__(kGateThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const uint32_t ep = p.lb ? s_ep : 0u;
+  if (threadIdx.x == 0) gate_tl(p, tl0, 1, 0);  // prologue done
 
   if (p.debug & 64) {  // dev: prologue + epilogue of the kernel only
   } else if (warp == 0) {
@@ -377,6 +394,7 @@ __global__ void __launch_bounds__(kGateThreads, 1)
         const int tile = kPair ? 2 * u + static_cast<int>(rank) : u;
         for (int kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
+          if (kb == 0 || kb == k_blocks - 1) gate_tl(p, tl0, kb == 0 ? 2 : 3, u);
           uint8_t* b = smem_b + stage * S::kBBytes;
           if constexpr (kPair) {
             const uint32_t fb = smem_u32(&full_bar[stage]) & kPeerMask;
@@ -417,10 +435,12 @@ __global__ void __launch_bounds__(kGateThreads, 1)
         const int acc = it & 1;
         mbar_wait(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
+        gate_tl(p, tl0, 4, u);
         const uint32_t d_tmem = tmem_base + acc * kAccCols;
         for (int kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
+          if (kb == 0) gate_tl(p, tl0, 5, u);
           const uint64_t adesc = umma_desc_k_sw128(smem_u32(smem_a + stage * S::kABytes));
 #pragma unroll
           for (int term = 0; term < (kCat ? 1 : kTerms); ++term) {
@@ -441,6 +461,7 @@ __global__ void __launch_bounds__(kGateThreads, 1)
         }
         if constexpr (kPair) umma_commit_2sm_mc(&tfull_bar[acc]);
         else umma_commit(&tfull_bar[acc]);
+        gate_tl(p, tl0, 6, u);
       }
     }
   } else if (kSplitEpi && warp >= 4) {
@@ -464,6 +485,7 @@ __global__ void __launch_bounds__(kGateThreads, 1)
       const bool valid = tile_ok && t < p.T;
       mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
       tc_fence_after();
+      if (lane == 0 && q == 0) gate_tl(p, tl0, 7 + half * 8, u);
       const int e0 = half * kHalf;
       const uint32_t t_row =
           tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * kAccCols + e0;
@@ -482,6 +504,7 @@ __global__ void __launch_bounds__(kGateThreads, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(smem_u32(&tempty_bar[acc]) & kPeerMask);
+          if (lane == 0 && q == 0) gate_tl(p, tl0, 8 + half * 8, u);
         }
         float v[16];
 #pragma unroll
@@ -528,6 +551,7 @@ __global__ void __launch_bounds__(kGateThreads, 1)
       named_bar_sync(3 + q, 64);  // half 1's partials are in shared memory
       if (half == 1) {
         named_bar_sync(7 + q, 64);  // group 0 has read them
+        if (lane == 0 && q == 0) gate_tl(p, tl0, 17, u);
         continue;
       }
       GateTop2 a0, a1;
@@ -610,6 +634,7 @@ __global__ void __launch_bounds__(kGateThreads, 1)
               for (int qq = 0; qq < 4; ++qq) h += cnt[(j * 4 + qq) * kGateMaxE + g];
             gate_publish_hist(p, j, tile, g, h, ep);
           }
+      if (lane == 0 && q == 0) gate_tl(p, tl0, 9, u);
     }
   } else if (warp >= 4) {
     const int q = warp & 3;
@@ -770,9 +795,11 @@ __global__ void __launch_bounds__(kGateThreads, 1)
     }
   }
 
+  if (threadIdx.x == 0 || threadIdx.x == 32 || threadIdx.x == 128) gate_tl(p, tl0, 10, warp);
   tc_fence_before();
   if constexpr (kPair) cluster_sync_all();
   else __syncthreads();
+  if (threadIdx.x == 0) gate_tl(p, tl0, 11, 0);
   if (warp == 2) {
     tc_fence_after();
     if constexpr (kPair)
@@ -783,7 +810,10 @@ __global__ void __launch_bounds__(kGateThreads, 1)
       tmem_dealloc<kTmemCols>(tmem_base);
   }
   if (p.lb) gate_fold_scan(p, ep);  // folded capacity scan (comoe_gate_route)
+  if (threadIdx.x == 0) gate_tl(p, tl0, 12, 0);
 }
+
+#include "gate_tm.cuh"
 
 template <int EP, bool kPair, int kTerms, int kStages>
 static int launch_gate_stages(const CUtensorMap& tx, const CUtensorMap& tw, const GateParams& p,
@@ -879,6 +909,18 @@ static int launch_gate(const CUtensorMap& tx, const CUtensorMap& tw, const GateP
                        cudaStream_t stream) {
   return gate_terms() == 3 ? launch_gate_terms<EP, kPair, 3>(tx, tw, p, stream)
                            : launch_gate_terms<EP, kPair, 2>(tx, tw, p, stream);
+}
+
+// Router-in-TMEM gate (gate_tm.cuh) for EP = 128, d <= 768: opt-in
+// (COMOE_GATE_TM=1, or comoe_debug_set_gate_tm at run time) — measured slower
+// than the pair kernel (K1, "router in tensor memory").
+static int g_gate_tm_override = -1;
+static bool gate_tm_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("COMOE_GATE_TM");
+    return e && e[0] == '1';
+  }();
+  return g_gate_tm_override >= 0 ? g_gate_tm_override != 0 : on;
 }
 
 static bool gate_pair_enabled() {
@@ -1167,8 +1209,17 @@ static int gate_launch(const void* x, int T, int d, const void* wg_split, int E,
     return e ? std::atoi(e) : 0;
   }();
   p.debug = dbg;
-  COMOE_REQUIRE(!(p.lb && dbg), kBadArg,
+  COMOE_REQUIRE(!(p.lb && (dbg & ~256)), kBadArg,
                 "gate_route: COMOE_GATE_DEBUG switches need comoe_gate_topk + comoe_route_scan");
+  if (EP == 128 && pair && gate_terms() == 2 && gate_tm_enabled() && d <= 768 && d % 128 == 0) {
+    CUtensorMap tx64, tr;
+    rc = make_tmap_bf16_2d(&tx64, x, T, d, 64);
+    if (rc) return rc;
+    // router rows [3 terms x 128, d], 16-row boxes (one TMEM lane half-quarter)
+    rc = make_tmap_bf16_2d_box(&tr, wg_split, 3ull * EP, d, d, 64, 16, 128);
+    if (rc) return rc;
+    return launch_gate_tm<8>(tx64, tr, p, s);
+  }
   switch (EP) {
     case 16: return pair ? launch_gate<16, true>(tx, tw, p, s) : launch_gate<16, false>(tx, tw, p, s);
     case 32: return pair ? launch_gate<32, true>(tx, tw, p, s) : launch_gate<32, false>(tx, tw, p, s);
@@ -1192,6 +1243,25 @@ int comoe_gate_topk(const void* x, int T, int d, const void* wg_split, int E, in
   return gate_launch(x, T, d, wg_split, E, top_k, norm_topk, slot_map, n_groups, logits_out,
                      expert_idx, group_idx, gate_prob, local_rank, tile_hist, GateParams{},
                      static_cast<cudaStream_t>(stream));
+}
+
+// dev: the gate timeline of CTAs 0 and 1 (COMOE_GATE_DEBUG bit 256), then
+// reset; out: [2][kGateTlMax] records, counts: [2]
+int comoe_debug_gate_timeline(unsigned long long* out, unsigned int* counts) {
+  using namespace comoe;
+  COMOE_REQUIRE(out && counts, kBadArg, "debug_gate_timeline: null pointer");
+  cudaError_t e = cudaMemcpyFromSymbol(out, g_gate_tl, sizeof(g_gate_tl));
+  counts[0] = counts[1] = kGateTlMax;
+  static unsigned long long zero[2][kGateTlMax];
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_gate_tl, zero, sizeof(zero));
+  COMOE_REQUIRE(e == cudaSuccess, kCudaError, "debug_gate_timeline: %s", cudaGetErrorString(e));
+  return kOk;
+}
+
+// dev: select the router-in-TMEM gate for later launches (1 on, 0 off, -1 env)
+int comoe_debug_set_gate_tm(int on) {
+  comoe::g_gate_tm_override = on;
+  return comoe::kOk;
 }
 
 long comoe_gate_route_workspace_bytes(int T, int top_k, int n_groups) {

@@ -338,17 +338,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k
     constexpr bool kTmaStore = kMode != kEpiScaleScatter;  // contiguous rows: TMA bulk store
     int nbuf = 0;
     int it = 0;
+    // chunks of one tile handled by this warp (ci = sub, sub + kSubs, ...)
+    constexpr int kMaxIt = (kBN / 32 + kSubs - 1) / kSubs;
     for (int tile = cluster; tile < total_tiles; tile += n_clusters, ++it) {
       const Tile2 t = decode_tile2<kBN>(prefix, p, f_tiles, tile);
       const int acc = it & 1;
       const long row_base = static_cast<long>(__ldg(p.group_row_base + t.g)) + t.tok0;
       const long col0 = static_cast<long>(t.ft) * k2BM + rank * 128 + q * 32;
+      // Scatter epilogue: the tile's gate probabilities and destination rows
+      // (lane = token c + lane of each chunk) are loaded before the wait on
+      // the accumulator, so their L2 latency hides behind the mainloop instead
+      // of sitting twice on every chunk's critical path (debug 4096: old form).
+      float pre_p[kMaxIt] = {};
+      int pre_t[kMaxIt] = {};
+      const bool preload = kMode == kEpiScaleScatter && !(p.debug & 4096);
+      if constexpr (kMode == kEpiScaleScatter) {
+        if (preload) {
+#pragma unroll
+          for (int i = 0; i < kMaxIt; ++i) {
+            const int tk = (sub + i * kSubs) * 32 + lane;
+            const bool ok = tk < t.ntok;
+            pre_p[i] = ok ? __ldg(p.row_prob + row_base + tk) : 0.f;
+            pre_t[i] = ok ? __ldg(p.row_token + row_base + tk) : 0;
+          }
+        }
+      }
       mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
       tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * kBN;
       const int chunks = (t.nmma + 31) >> 5;
       bool released = false;
-      for (int ci = sub; ci < chunks; ci += kSubs) {
+#pragma unroll
+      for (int i = 0; i < kMaxIt; ++i) {
+        const int ci = sub + i * kSubs;
+        if (ci >= chunks) break;
         const int c = ci * 32;
         uint32_t v[32];
         tmem_ld32(t_row + c, v);
@@ -365,7 +388,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(fmaxf(__uint_as_float(v[j]), 0.f));
         } else if constexpr (kMode == kEpiScaleScatter) {
-          const float my_p = (c + lane < t.ntok) ? __ldg(p.row_prob + row_base + c + lane) : 0.f;
+          const float my_p = preload ? pre_p[i]
+                                     : ((c + lane < t.ntok) ? __ldg(p.row_prob + row_base + c + lane) : 0.f);
 #pragma unroll
           for (int j = 0; j < 32; ++j)
             v[j] = __float_as_uint(__uint_as_float(v[j]) * __shfl_sync(0xffffffffu, my_p, j));
@@ -412,13 +436,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k
         }
         if (!stored) {  // scatter rows or a partial chunk: 16-B stores, 4 lanes per row
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int r = 8 * i + (lane >> 2), j = lane & 3;
+          for (int ii = 0; ii < 4; ++ii) {
+            const int r = 8 * ii + (lane >> 2), j = lane & 3;
             const uint4 x = lds128(sg + r * 64 + ((j ^ ((r >> 1) & 3)) << 4));
             const int tk = c + r;
+            int pre_dst = 0;
+            if constexpr (kMode == kEpiScaleScatter) pre_dst = __shfl_sync(0xffffffffu, pre_t[i], r);
             if (tk < t.ntok && !(p.debug & 512)) {
               long dst;
-              if constexpr (kMode == kEpiScaleScatter) dst = __ldg(p.row_token + row_base + tk);
+              if constexpr (kMode == kEpiScaleScatter)
+                dst = preload ? pre_dst : __ldg(p.row_token + row_base + tk);
               else dst = row_base + tk;
               if (p.debug & 2048) dst = r;  // dev: every tile writes the same 32 rows (L2-resident)
               st_global_v4(p.out + dst * p.ldo + col0 + j * 8, x.x, x.y, x.z, x.w);

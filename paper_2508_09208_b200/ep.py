@@ -118,7 +118,7 @@ def ep_chunk_base(n_groups: int, world: int, capacity: int, chunks: int, device=
 
 
 def ep_forward(x, ops, world: int, n_experts: int, capacity: int, group=None, stage=None,
-               chunks: int = 1):
+               chunks: int = 1, out=None):
     """One EP layer forward of this rank's tokens `x` [T_g, d]. `stage`:
     optional callable(name) -> context manager timing each step (bench.py).
 
@@ -128,7 +128,8 @@ def ep_forward(x, ops, world: int, n_experts: int, capacity: int, group=None, st
     k's grouped FFN runs as soon as its rows have arrived — while chunk
     k+1's rows are still in flight — and its outputs go back asynchronously
     while chunk k+1 computes. Each expert's weights are still read once per
-    chunk it belongs to, i.e. once."""
+    chunk it belongs to, i.e. once. `out`: optional [T_g, d] tensor the
+    combine writes into (no extra copy)."""
     st = stage if stage is not None else (lambda name: _NoStage())
     E, C = n_experts, capacity
     El = E // world
@@ -149,7 +150,7 @@ def ep_forward(x, ops, world: int, n_experts: int, capacity: int, group=None, st
             y_back = torch.empty_like(y_recv)
             dist.all_to_all_single(y_back, y_recv, group=group)
         with st("combine"):
-            return ops.combine(y_back, token_pos, route)
+            return ops.combine(y_back, token_pos, route, out=out)
     Lc = El // chunks
     base = ep_chunk_base(E, world, C, chunks, x.device)
     with st("permute"):
@@ -179,7 +180,7 @@ def ep_forward(x, ops, world: int, n_experts: int, capacity: int, group=None, st
         for w in backs:
             w.wait()
     with st("combine"):
-        return ops.combine(y_back, token_pos, route)
+        return ops.combine(y_back, token_pos, route, out=out)
 
 
 class PeerBuffers:
@@ -261,7 +262,8 @@ class PeerBuffers:
         self._opened = []
 
 
-def ep_forward_peers(x, ops, bufs: PeerBuffers, n_experts: int, capacity: int, stage=None):
+def ep_forward_peers(x, ops, bufs: PeerBuffers, n_experts: int, capacity: int, stage=None,
+                     out=None):
     """ep_forward with the all-to-alls replaced by peer-memory stores and
     loads: permute into the owners' receive buffers (+ counts), barrier,
     grouped FFN into my output buffer, barrier, combine from the owners'
@@ -280,7 +282,7 @@ def ep_forward_peers(x, ops, bufs: PeerBuffers, n_experts: int, capacity: int, s
     with st("a2a_combine"):
         bufs.barrier()
     with st("combine"):
-        return ops.combine_peers(token_pos, route, bufs)
+        return ops.combine_peers(token_pos, route, bufs, out=out)
 
 
 class DeviceOps:
@@ -342,9 +344,9 @@ class DeviceOps:
         kernels.peer_scatter_counts(route.kept, bufs.world, bufs.rank, bufs.counts_ptrs)
         return perm.token_pos
 
-    def combine_peers(self, token_pos, route, bufs):
+    def combine_peers(self, token_pos, route, bufs, out=None):
         return kernels.combine_peers(bufs.y_ptrs, bufs.block_rows, bufs.rank, token_pos,
-                                     route.gate.gate_prob, bufs.d)
+                                     route.gate.gate_prob, bufs.d, out=out)
 
     def expert_ffn(self, recv_rows, recv_counts, El, C, world, stage=None, y_out=None,
                    slot_offset: int = 0):
@@ -391,8 +393,8 @@ class DeviceOps:
                                  kernels.EPI_STORE, y)
         return y
 
-    def combine(self, y_back, token_pos, route):
-        return kernels.combine(y_back, token_pos, route.gate.gate_prob)
+    def combine(self, y_back, token_pos, route, out=None):
+        return kernels.combine(y_back, token_pos, route.gate.gate_prob, out=out)
 
 
 class EPMoELayer:
@@ -489,17 +491,14 @@ class EPMoELayer:
         C = self.capacity(x.shape[0])
         if self.transport == "peer":
             bufs = self.peer_buffers(x.shape[0])
-            y = ep_forward_peers(x, self.ops, bufs, self.G_pad, C, stage=timer)
+            y = ep_forward_peers(x, self.ops, bufs, self.G_pad, C, stage=timer, out=out)
             self._calls = getattr(self, "_calls", 0) + 1
             if self._calls % self.err_check_every == 0 and \
                     not torch.cuda.is_current_stream_capturing():
                 bufs.check()
         else:
             y = ep_forward(x, self.ops, self.world, self.G_pad, C, group=self.group, stage=timer,
-                           chunks=self.chunks)
-        if out is not None:
-            out.copy_(y)
-            return out
+                           chunks=self.chunks, out=out)
         return y
 
     __call__ = forward

@@ -49,6 +49,15 @@ def _need(t: torch.Tensor, name: str, dtype=None, dims=None, align=16):
     return t
 
 
+def _need_out(out: torch.Tensor, shape, device):
+    """An output tensor handed in by the caller: bf16, `shape`, on `device`."""
+    _need(out, "out", torch.bfloat16, len(shape))
+    if tuple(out.shape) != tuple(shape):
+        raise ValueError(f"out must have shape {tuple(shape)}, got {tuple(out.shape)}")
+    if out.device != device:
+        raise ValueError(f"out must live on {device}, got {out.device}")
+
+
 def num_sms(device=None) -> int:
     dev = torch.cuda.current_device() if device is None else device
     return _lib.load().comoe_num_sms(int(dev))
@@ -246,6 +255,7 @@ def combine(y_perm, token_pos, gate_prob, out=None) -> torch.Tensor:
     d = y_perm.shape[1]
     if out is None:
         out = torch.empty((T, d), dtype=torch.bfloat16, device=y_perm.device)
+    _need_out(out, (T, d), y_perm.device)
     _lib.call("comoe_combine", _ptr(y_perm), _ptr(token_pos), _ptr(gate_prob), T, d, k,
               _ptr(out), _stream())
     return out
@@ -280,6 +290,7 @@ def combine_peers(peer_rows, block_rows: int, src_rank: int, token_pos, gate_pro
     T, k = token_pos.shape
     if out is None:
         out = torch.empty((T, d), dtype=torch.bfloat16, device=token_pos.device)
+    _need_out(out, (T, d), token_pos.device)
     _lib.call("comoe_combine_peers", _ptr(peer_rows), peer_rows.numel(), int(block_rows),
               int(src_rank), _ptr(token_pos), _ptr(gate_prob), T, d, k, _ptr(out), _stream())
     return out

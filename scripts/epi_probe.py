@@ -30,15 +30,19 @@ f3 = lambda: kernels.grouped_gemm(ws["h"], pool.data, F * D, D, r.scan.group_kep
                                   layer.group_slot, kernels.EPI_STORE, ws["y_perm_probe"])
 ws["y_perm_probe"] = torch.empty_like(x)
 out = {"debug": os.environ.get("COMOE_GEMM_DEBUG", "0")}
+only = os.environ.get("EPI_ONLY")  # one GEMM only (for ncu: EPI_ONLY=gemm2_scatter REPS=1)
+reps = int(os.environ.get("REPS", "10"))
 for name, f in (("gemm1_relu_tma", f1), ("gemm2_scatter", f2), ("gemm2_store_tma", f3)):
+    if only and name != only:
+        continue
     for _ in range(3):
         f()
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
-    for _ in range(10):
+    for _ in range(reps):
         f()
     b.record()
     torch.cuda.synchronize()
-    out[name] = round(a.elapsed_time(b) / 10 * 1e3, 1)
+    out[name] = round(a.elapsed_time(b) / reps * 1e3, 1)
 print(json.dumps(out))

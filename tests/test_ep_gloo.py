@@ -81,13 +81,16 @@ class OracleOps:
                 out[g * C:g * C + n] = torch.from_numpy(y.astype(np.float32))
         return out
 
-    def combine(self, y_back, token_pos, route):
+    def combine(self, y_back, token_pos, route, out=None):
         yb = y_back.numpy()
         T = token_pos.shape[0]
         y = np.zeros((T, yb.shape[1]), np.float64)
         for j in range(self.top_k):
             m = token_pos[:, j] >= 0
             y[m] += route.prob[m, j][:, None] * yb[token_pos[m, j]]
+        if out is not None:
+            out.copy_(torch.from_numpy(y))
+            return out
         return torch.from_numpy(y)
 
 

@@ -116,3 +116,46 @@ def test_gate_route_workspace_checked():
     small = torch.zeros(4, dtype=torch.int64, device="cuda")
     with pytest.raises(ValueError):
         kernels.gate_route(x, split, 8, 1, False, 160, small)
+
+
+@pytest.mark.parametrize("T,top_k,d,cf", [(65536, 1, 768, 1.25), (3000, 1, 512, 1.25),
+                                          (5000, 2, 768, 2.0), (1, 1, 768, 1.25)])
+def test_router_in_tmem_gate(T, top_k, d, cf):
+    """The opt-in router-in-TMEM gate (gate_tm.cuh, E = 128) against the
+    oracle on its own device logits (routing, probabilities, stream-order
+    dispatch), and its logits against the default pair gate's (the two
+    kernels accumulate x.hi and x.mid in transposed MMA shapes)."""
+    from paper_2508_09208_b200 import _lib, kernels
+    E = 128
+    x, wg = _inputs(T, d, E, seed=T + d)
+    split = kernels.gate_prepare(wg)
+    C = kernels.capacity_for(T, E, top_k, cf)
+    out = []
+    try:
+        for tm in (0, 1):
+            _lib.call("comoe_debug_set_gate_tm", tm)
+            ws = kernels.gate_route_workspace(T, top_k, E, x.device)
+            g, s = kernels.gate_route(x, split, E, top_k, top_k == 2, C, ws, n_groups=E,
+                                      want_logits=True)
+            torch.cuda.synchronize()
+            out.append((g, s))
+    finally:
+        _lib.call("comoe_debug_set_gate_tm", -1)
+    (g0, _), (g1, s1) = out
+    torch.testing.assert_close(g1.logits, g0.logits, rtol=0, atol=2e-6)
+    idx, group, prob = O.topk_route(g1.logits.cpu().numpy(), top_k, top_k == 2)
+    np.testing.assert_array_equal(g1.expert_idx.cpu().numpy(), idx)
+    np.testing.assert_array_equal(g1.group_idx.cpu().numpy(), group)
+    np.testing.assert_allclose(g1.gate_prob.cpu().numpy(), prob, rtol=2e-5, atol=1e-7)
+    disp = O.dispatch_fast(group, E, C)
+    np.testing.assert_array_equal(s1.group_count.cpu().numpy(), disp["count"])
+    np.testing.assert_array_equal(s1.group_kept.cpu().numpy(), disp["kept"])
+    np.testing.assert_array_equal(s1.group_base.cpu().numpy(), disp["base"])
+    # stream-order rank = the tile's offset for the group + the in-tile rank
+    lr = g1.local_rank.cpu().numpy()
+    to = s1.tile_offset.cpu().numpy()  # [k][tiles][G]
+    tok = np.arange(T)
+    for j in range(top_k):
+        m = group[:, j] >= 0
+        got = to[j, tok[m] // 128, group[m, j]] + lr[m, j]
+        np.testing.assert_array_equal(got, disp["rank"][m, j])
