@@ -75,6 +75,7 @@ struct GateParams {
   int* group_kept;        // [G]
   int* group_base;        // [G]
   int capacity;
+  int xpol;  // dev: L2 policy of the x loads (0 evict_last, 1 normal, 2 first)
 };
 
 // ------------------------------------------------------------ folded scan
@@ -386,7 +387,9 @@ __global__ void __launch_bounds__(kGateThreads, 1)
   } else if (warp == 0) {
     if (elect_one()) {
       // keep x in L2: the permute re-reads every row right after the gate
-      const uint64_t pol_x = l2_policy_evict_last();
+      // (dev: COMOE_GATE_XPOL=1 evict_normal, 2 evict_first)
+      const uint64_t pol_x = p.xpol == 2 ? l2_policy_evict_first()
+                             : p.xpol == 1 ? l2_policy_evict_normal() : l2_policy_evict_last();
       const uint64_t pol_w = l2_policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
@@ -1209,6 +1212,11 @@ static int gate_launch(const void* x, int T, int d, const void* wg_split, int E,
     return e ? std::atoi(e) : 0;
   }();
   p.debug = dbg;
+  static const int xpol = [] {
+    const char* e = std::getenv("COMOE_GATE_XPOL");
+    return e ? std::atoi(e) : 0;
+  }();
+  p.xpol = xpol;
   COMOE_REQUIRE(!(p.lb && (dbg & ~256)), kBadArg,
                 "gate_route: COMOE_GATE_DEBUG switches need comoe_gate_topk + comoe_route_scan");
   if (EP == 128 && pair && gate_terms() == 2 && gate_tm_enabled() && d <= 768 && d % 128 == 0) {

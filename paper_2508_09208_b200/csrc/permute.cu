@@ -6,6 +6,8 @@
 // has rank = tokens before it in stream order (all first choices in token
 // order, then all second choices); it is kept iff rank < capacity and lands
 // at row base[g] + rank of the compact, expert-sorted buffer.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "../../include/comoe_b200.h"
 
@@ -30,6 +32,7 @@ struct PermuteParams {
   // block_rows), i.e. the all-to-all is the store itself
   __nv_bfloat16* const* peer_rows;
   int block_rows, src_off;
+  int rev;  // dev (COMOE_PERMUTE_REV=1): walk the tokens last-to-first
 };
 
 // Row address of destination row `dest` in the local buffer or, with peers,
@@ -60,8 +63,9 @@ __global__ void __launch_bounds__(256, 3) permute_kernel(PermuteParams p) {
   const int lane = threadIdx.x & 31;
   const int vec = p.d >> 3;  // uint4 per row
   const bool copy = kPeers || p.x_perm != nullptr;
-  for (int t0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kTokPerWarp; t0 < p.T;
-       t0 += warps * kTokPerWarp) {
+  const int nb = (p.T + kTokPerWarp - 1) / kTokPerWarp;
+  for (int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < nb; b += warps) {
+    const int t0 = (p.rev ? nb - 1 - b : b) * kTokPerWarp;
     int4 v[kTokPerWarp][kRowUnroll];
     auto load_slice = [&](int i0) {
 #pragma unroll
@@ -242,6 +246,11 @@ int comoe_permute(const void* x, int T, int d, int top_k, const int* group_idx,
                   (T + 127) / 128, group_idx, gate_prob, local_rank, tile_offset, group_base,
                   reinterpret_cast<__nv_bfloat16*>(x_perm), row_token, row_prob, token_pos,
                   reinterpret_cast<__nv_bfloat16*>(y_zero), nullptr, 0, 0};
+  static const int rev = [] {
+    const char* e = std::getenv("COMOE_PERMUTE_REV");
+    return e && e[0] == '1' ? 1 : 0;
+  }();
+  p.rev = rev;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid_for_warps((T + kTokPerWarp - 1) / kTokPerWarp));
   cfg.blockDim = dim3(256);
