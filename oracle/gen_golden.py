@@ -23,6 +23,11 @@ Fixtures
                        demote / evict) on a small scenario + its inputs
   traces.json          generate_routing traces (+ the reference's
                        collect_stats of each) and a trained predictor
+  library_cases.json   build_library over two-layer models: every variant's
+                       groups / slot map / sizes / score, variant_freqs,
+                       library_manifest, select_variant at several memory
+                       levels, plus should_switch and granularity_decision
+                       cases (values and error cases)
 """
 
 from __future__ import annotations
@@ -352,6 +357,89 @@ def cache_parity(moe):
                     late_prefetch_count=report.late_prefetch_count))
 
 
+def library_cases(moe, agg, n_cases=12):
+    rng = np.random.default_rng(20261017)
+    cases = []
+    for i in range(n_cases):
+        E = int(rng.integers(3, 13))
+        dim = 16
+        scope = "both" if i % 3 == 2 else "encoder"
+        spec = moe.MoeModelSpec(total_layers=4, encoder_moe_layers=(1,), decoder_moe_layers=(3,),
+                                experts_per_layer=E, expert_size_bytes=float(rng.choice([1e6, 2.5e6])),
+                                top_k=1, expert_param_dim=dim)
+        model = moe.synthesize_model(spec, int(rng.integers(0, 2 ** 31)))
+        counts = {}
+        for layer in (1, 3):
+            c = rng.integers(0, 40, size=E).astype(float)
+            if c.sum() == 0:
+                c[0] = 1.0
+            if i % 4 == 1:
+                c[1 % E] = c[0]  # frequency ties
+            counts[layer] = c
+        stats = moe.ActivationStats(counts=counts, totals={l: int(c.sum()) for l, c in counts.items()},
+                                    experts_per_layer=E)
+        calib = moe.make_calibration(dim, n_probes=4, seed=int(rng.integers(0, 1000)), buckets=4)
+        alpha = float(rng.choice([0.0, 0.5, 1.0]))
+        m_other = float(rng.choice([0.0, 3e6]))
+        configs = [agg.FusionConfig(mode="fixed", r=0.5, scope=scope),
+                   agg.FusionConfig(mode="fixed", r=0.25, theta_act=0.05, scope=scope),
+                   agg.FusionConfig(mode="adaptive", r_base=0.5, delta_r=0.25, e_min=1, scope=scope)]
+        lib = agg.build_library(model, stats, configs, alpha, calib, m_other)
+        variants = []
+        for v in lib.variants:
+            variants.append(dict(
+                id=v.variant_id, mem_required=v.mem_required, expert_bytes=v.expert_bytes,
+                perf_estimate=v.perf_estimate,
+                slot_map={str(l): {str(k): int(x) for k, x in m.items()} for l, m in v.slot_map.items()},
+                groups={str(l): [[g.principal_slot, list(g.member_slots)] for g in gs]
+                        for l, gs in v.groups.items()},
+                freqs=[[int(l), int(sl), float(f)] for (l, sl), f in
+                       sorted(agg.variant_freqs(v, stats).items())]))
+        mems = sorted({v.mem_required for v in lib.variants})
+        levels = [mems[0] * 0.5] + mems + [0.5 * (a + b) for a, b in zip(mems, mems[1:])] + [mems[-1] * 2]
+        selects = []
+        for m in levels:
+            try:
+                selects.append([m, agg.select_variant(lib, m).variant_id])
+            except Exception as exc:  # infeasible
+                selects.append([m, type(exc).__name__])
+        cases.append(dict(E=E, scope=scope, alpha=alpha, m_other=m_other,
+                          params={str(l): [e.params.tolist() for e in model.layer_experts(l)]
+                                  for l in (1, 3)},
+                          sizes={str(l): [e.size for e in model.layer_experts(l)] for l in (1, 3)},
+                          counts={str(l): c.tolist() for l, c in counts.items()},
+                          probes=calib.probes.tolist(), projection=calib.projection.tolist(),
+                          variants=variants, manifest=agg.library_manifest(lib), selects=selects))
+    switch = []
+    for _ in range(40):
+        a = agg.ModelVariant(variant_id=str(rng.choice(["a", "b"])), retained={}, slot_map={},
+                             groups={}, mem_required=1.0, perf_estimate=0.5)
+        b = agg.ModelVariant(variant_id=str(rng.choice(["a", "b", "c"])), retained={}, slot_map={},
+                             groups={}, mem_required=1.0, perf_estimate=0.5)
+        pol = agg.SwitchPolicy(lambda_switch=float(rng.choice([0.0, 0.5, 1.0])),
+                               switch_cost=float(rng.choice([0.0, 0.05, 0.2])),
+                               t_threshold=float(rng.choice([0.0, 4.0, 8.0])))
+        dp = float(rng.choice([0.0, 0.01, 0.025, 0.1, 0.5]))
+        ts = float(rng.choice([-1.0, 0.0, 4.0, 8.0, 9.0]))
+        try:
+            out = bool(agg.should_switch(a, b, dp, pol, ts))
+        except ValueError:
+            out = "ValueError"
+        switch.append(dict(cur=a.variant_id, cand=b.variant_id, delta_p=dp, lambda_switch=pol.lambda_switch,
+                           switch_cost=pol.switch_cost, t_threshold=pol.t_threshold, t_stable=ts, out=out))
+    gran = []
+    for _ in range(40):
+        args = (float(rng.choice([0.0, 0.3, 0.7, 0.95, 1.0])), float(rng.choice([1e9, 8e9, 80e9])),
+                float(rng.choice([0.0, 9.4e6, 4.7e8])), float(rng.choice([0.0, 0.5, 2.0])),
+                float(rng.choice([-0.1, 0.0, 0.4, 1.0])), int(rng.choice([8, 64, 128])))
+        try:
+            out = int(agg.granularity_decision(*args))
+        except ValueError:
+            out = "ValueError"
+        gran.append(dict(args=list(args), out=out))
+    return dict(cases=cases, should_switch=switch, granularity=gran)
+
+
 def main():
     moe, agg, off = _ref()
     (OUT / "cache_parity.json").write_text(json.dumps(cache_parity(moe)))
@@ -362,6 +450,7 @@ def main():
     (OUT / "merge_hand.json").write_text(json.dumps(merge_hand(moe, agg), indent=1))
     (OUT / "merge_bigsum.json").write_text(json.dumps(merge_bigsum(moe, agg), indent=1))
     (OUT / "policy_cases.json").write_text(json.dumps(policy_cases(off)))
+    (OUT / "library_cases.json").write_text(json.dumps(library_cases(moe, agg)))
     for p in sorted(OUT.glob("*.json")):
         print(p.name, p.stat().st_size)
 
