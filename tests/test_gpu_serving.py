@@ -64,6 +64,15 @@ def test_expert_parallel_world1_matches_oracle():
         yc = layer_c.forward(x.cuda())
         torch.cuda.synchronize()
         assert torch.equal(yc, y), chunks
+        # out=: the combine writes the caller's buffer (no extra copy)
+        yo = torch.full_like(y, float("nan"))
+        assert layer_c.forward(x.cuda(), out=yo) is yo
+        torch.cuda.synchronize()
+        assert torch.equal(yo, y), chunks
+    yo = torch.empty_like(y)
+    assert layer.forward(x.cuda(), out=yo) is yo
+    torch.cuda.synchronize()
+    assert torch.equal(yo, y)
     torch.cuda.synchronize()
     logits = None
     wi = np.stack([O.split_expert(w[e].float().numpy(), d, d_ff, "relu")[0] for e in range(E)])
