@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -54,7 +56,7 @@ __global__ void __launch_bounds__(32, 1) stream_kernel(const __grid_constant__ C
     if (i >= 0) wait_bar(&bar[i % stages], (i / stages) & 1);
 }
 
-int main() {
+int main(int argc, char** argv) {
   const long bytes = 2L << 30;
   char* buf;
   cudaMalloc(&buf, bytes);
@@ -65,7 +67,13 @@ int main() {
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   // Gram-like: 128 rows (whole experts) of `pitch` bytes, boxes walk the columns
-  for (long pitch : {9437184L, 4L << 20, 2L << 20, 1572864L, 1L << 20, 512L << 10, 256L << 10, 64L << 10}) {
+  // argv: pitches (bytes) of the gram-like sweep; default: the round-2 set
+  std::vector<long> pitches = {9437184L, 4L << 20, 2L << 20, 1572864L, 1L << 20, 512L << 10, 256L << 10, 64L << 10};
+  if (argc > 1) {
+    pitches.clear();
+    for (int i = 1; i < argc; ++i) pitches.push_back(std::atol(argv[i]));
+  }
+  for (long pitch : pitches) {
     const long rows = 128, cols = (bytes / rows / 1024) * 512;  // row length in elements
     CUtensorMap map{};
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
@@ -95,7 +103,7 @@ int main() {
            3.0 * iters * (double)sms * 16384 / (ms * 1e-3) / 1e12);
     (void)cols;
   }
-  for (int mode = 0; mode < 2; ++mode)
+  for (int mode = 0; mode < (argc > 1 ? 0 : 2); ++mode)
     for (long pitch : {128L, 1536L, 6144L}) {
       if (mode == 0 && pitch != 128) continue;
       const long cols = pitch / 2, rows = bytes / pitch;
