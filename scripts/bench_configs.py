@@ -61,8 +61,15 @@ def run_config(name, d, d_ff, E, top_k, act, T, ratios, calib_kind):
     out = []
     ms = timed(lambda: layer.forward(x))
     flops = 2.0 * T * top_k * (numel)
+    # device time: the same forward as one CUDA-graph replay (no per-launch
+    # host overhead, which dominates the eager small-batch C1 figure)
+    y = torch.empty_like(x)
+    cap = layer.capture(x, y)
+    ms_g = timed(cap.replay, reps=20)
     out.append({"config": name, "variant": f"original-{E}", "tokens": T, "ms": ms,
-                "tokens_per_s": T / ms * 1e3, "expert_tflops": flops / ms / 1e9})
+                "tokens_per_s": T / ms * 1e3, "expert_tflops": flops / ms / 1e9,
+                "graph_ms": ms_g, "graph_tokens_per_s": T / ms_g * 1e3,
+                "graph_expert_tflops": flops / ms_g / 1e9})
     # activation statistics from the device router
     r = layer.route(x)
     stats = stats_from_routing({1: r.gate.expert_idx}, E)
@@ -101,7 +108,10 @@ def run_config(name, d, d_ff, E, top_k, act, T, ratios, calib_kind):
         var = A.fuse_model(model, stats, cfg, alpha, calib, pool=pool)
         layer.use_variant(var, 1)
         ms_v = timed(lambda: layer.forward(x))
+        cap_v = layer.capture(x, y)
+        ms_vg = timed(cap_v.replay, reps=20)
         out.append({"config": name, "variant": var.variant_id, "experts_after": target,
+                    "graph_ms": ms_vg, "graph_tokens_per_s": T / ms_vg * 1e3,
                     "groups": {g_.principal_slot: list(g_.member_slots) for g_ in groups},
                     "similarity_ms": sim_ms, "similarity_first_call_ms": sim_first_ms,
                     "merge_ms": merge_ms, "merge_bytes": mbytes,

@@ -1,7 +1,8 @@
 """C2 layer: one CUDA-graph replay of the forward against the sum of its
 kernels, each timed alone back to back (dev probe): the difference is what
 kernel boundaries cost inside the graph (launch latency, prologue, ramp-up /
-tail). Run once per COMOE_PDL setting. One JSON line, µs."""
+tail). Run once per COMOE_PDL setting; env T / E pick the batch and the
+expert count (default the C2 shape; T=4096 E=8 is C1). One JSON line, µs."""
 import json
 import math
 import os
@@ -12,7 +13,9 @@ import torch
 
 from paper_2508_09208_b200 import ExpertPool, MoELayer, kernels
 
-T, D, F, E = 65536, 768, 3072, 128
+T = int(os.environ.get("T", "65536"))
+E = int(os.environ.get("E", "128"))
+D, F = 768, 3072
 dev = torch.device("cuda")
 g = torch.Generator(device=dev).manual_seed(0)
 x = torch.randn(T, D, device=dev, generator=g).to(torch.bfloat16)
@@ -56,4 +59,5 @@ out["ffn2_us"] = timed(lambda: kernels.grouped_gemm(ws["h"], pool.data, F * D, D
 out["sum_us"] = out["route_us"] + out["permute_us"] + out["ffn1_us"] + out["ffn2_us"]
 out["graph_minus_sum_us"] = out["graph_us"] - out["sum_us"]
 out["env"] = {k: v for k, v in os.environ.items() if k.startswith("COMOE_")}
+out["T"], out["E"] = T, E
 print(json.dumps({k: (round(v, 1) if isinstance(v, float) else v) for k, v in out.items()}))
