@@ -446,6 +446,38 @@ def run_ours(args):
         # the kernel, profiles/r1_gemm_clock.jsonl), the sustained regime
         roofline["frac_vs_sustained_peak"] = achieved / sustained
         roofline["sustained_peak"] = sustained
+    # the SM clock inside the dominant GEMM: a few eager forwards right after
+    # the timed loop with COMOE_GEMM_DEBUG bit 256 set at run time (CTA 0 of
+    # the output GEMM stamps clock64 and the global ns timer at entry and
+    # exit); the tensor pipe's peak at that clock is 4096 MAC/clk/SM
+    # (scripts/mma_peak.cu), so frac_at_clock separates kernel efficiency
+    # from the power cap's frequency
+    if dom in ("ffn1", "ffn2") and world == 1 and not args.force_ep and achieved is not None:
+        import ctypes
+        import statistics
+        from paper_2508_09208_b200 import _lib
+        mhz = []
+        try:
+            _lib.call("comoe_debug_set_gemm", 256)
+            for _ in range(5):
+                layer.forward(x, out=y)
+                torch.cuda.synchronize()
+                buf = (ctypes.c_ulonglong * 4)()
+                _lib.call("comoe_debug_gemm_clock", buf)
+                if buf[3] > buf[1]:
+                    mhz.append((buf[2] - buf[0]) / (buf[3] - buf[1]) * 1e3)
+        finally:
+            _lib.call("comoe_debug_set_gemm", -1)
+        if mhz:
+            f = statistics.median(mhz)
+            peak_f = 2 * 4096 * 148 * f * 1e6 / 1e12
+            roofline["at_kernel_clock"] = {
+                "sm_mhz_in_kernel": f, "samples": len(mhz), "peak_at_clock": peak_f,
+                "frac_at_clock": achieved / peak_f,
+                "note": "SM clock read inside the output GEMM (CTA 0 clock64 / globaltimer; the "
+                        "two GEMMs run back to back under the same power cap) on eager forwards "
+                        "right after the timed loop; peak = 4096 MAC/clk/SM x 148 SMs at that "
+                        "clock (scripts/mma_peak.cu)"}
     # the roof this kernel actually presses on: operand bytes each
     # SM ingests from L2 per launch (ncu, committed) over the live launch time,
     # against the measured per-SM ingest ceiling (scripts/l2_probe.cu)
