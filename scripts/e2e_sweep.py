@@ -26,12 +26,16 @@ layer = MoELayer(wg, pool, d_ff, capacity_factor=1.25)
 xh = x.cpu().pin_memory()
 yhs = [torch.empty_like(xh).pin_memory() for _ in range(3)]
 steps = int(os.environ.get("STEPS", "20"))
-for depth, chunks, cs in itertools.product((2, 3), (2, 4, 8, 16), (1, 2, 4)):
-    pipe = HostPipeline(layer, T, d, depth=depth, device=dev, chunks=chunks, copy_streams=cs)
+grid = os.environ.get("GRID")  # e.g. "2:1:1,2:4:2" = depth:chunks:streams
+combos = ([tuple(int(v) for v in c.split(":")) for c in grid.split(",")] if grid else
+          itertools.product((2, 3), (1, 2, 4, 8, 16), (1, 2, 4)))
+for depth, chunks, cs in combos:
+    pipe = HostPipeline(layer, T, d, depth=depth, device=dev, chunks=chunks, copy_streams=cs,
+                        graphs=os.environ.get("GRAPHS", "1") == "1")
     pipe.run([xh] * 3, [yhs[i % 3] for i in range(3)])
     pipe.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     pipe.run([xh] * steps, [yhs[i % 3] for i in range(steps)], start_event=s, end_event=e)
     pipe.synchronize()
-    print(json.dumps({"depth": depth, "chunks": chunks, "copy_streams": cs,
+    print(json.dumps({"depth": depth, "chunks": chunks, "copy_streams": cs, "steps": steps,
                       "ms_per_step": s.elapsed_time(e) / steps}), flush=True)
