@@ -258,7 +258,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k
       // 128 = slot 0 only — L2-resident operands; +27-42% / +17% at C2)
       const int slot = (p.debug & (16 | 128)) ? 0 : __ldg(p.group_slot + t.g);
       const int feat = t.ft * k2BM + static_cast<int>(rank) * 128;
-      const int gbase = (p.debug & 16) ? -t.tok0 : __ldg(p.group_row_base + t.g);
+      // (dev 32768: token rows only L2-resident — every tile reads rows 0..255;
+      // the weights still stream from HBM)
+      const int gbase = (p.debug & (16 | 32768)) ? -t.tok0 : __ldg(p.group_row_base + t.g);
       const int half0 = t.tok0 + static_cast<int>(rank) * (t.nmma >> 1);
       int idx0 = 0, idx1 = 0, idx2 = 0, idx3 = 0;
       if constexpr (kGather) {

@@ -54,7 +54,9 @@ for rnd in range(int(os.environ.get("ROUNDS", "3"))):
                 f()
             b.record()
             torch.cuda.synchronize()
-            print(json.dumps({"round": rnd, "gemm": name, "debug": m,
-                              "us": round(a.elapsed_time(b) / reps * 1e3, 1),
-                              "mhz_last": round(mhz(), 0)}), flush=True)
+            us = a.elapsed_time(b) / reps * 1e3
+            clk = mhz()
+            print(json.dumps({"round": rnd, "gemm": name, "debug": m, "us": round(us, 1),
+                              "mhz_last": round(clk, 0), "kcycles": round(us * clk / 1e3, 1)}),
+                  flush=True)
 _lib.call("comoe_debug_set_gemm", -1)
