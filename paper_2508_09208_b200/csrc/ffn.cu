@@ -233,6 +233,17 @@ static int ft_major(long weight_bytes) {
   return weight_bytes > (32L << 20) ? 1 : 0;
 }
 
+// Equal token tiles for the 2-SM kernel when K >= 1536 (COMOE_GEMM_EQUAL=0/1
+// forces off/on): see decode_tile2.
+static int equal_tiles(int K) {
+  static const int forced = [] {
+    const char* e = std::getenv("COMOE_GEMM_EQUAL");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (forced >= 0) return forced;
+  return K >= 1536 ? 1 : 0;
+}
+
 static bool force_1sm() {
   static const bool f = [] {
     const char* e = std::getenv("COMOE_GEMM_1SM");
@@ -266,7 +277,8 @@ static int grouped_gemm_impl(const void* a, long a_rows, const void* pool, int n
   const void* b = static_cast<const __nv_bfloat16*>(pool) + b_offset;
   GroupedGemmParams p{group_rows, group_row_base, group_slot, G, N, K,
                       reinterpret_cast<__nv_bfloat16*>(out), ldo, row_token, row_prob,
-                      a_gather, gemm_debug(), ft_major(static_cast<long>(N) * K * 2)};
+                      a_gather, gemm_debug(), ft_major(static_cast<long>(N) * K * 2),
+                      equal_tiles(K)};
   int rc;
   // SwiGLU stays on the 1-SM kernel: a 2-SM variant (gate/up rows split into
   // 64-row boxes per SM, up values handed to the gate warps through shared

@@ -43,6 +43,8 @@ struct GroupedGemmParams {
                           // 16/128 = L2-resident operands (see the producer); 0 in production
   int ft_major;           // tile order inside a group (0: token tile major,
                           // 1: feature tile major — consecutive CTAs share a weight tile)
+  int equal_tiles;        // 2-SM kernel: split a group's rows into equal token tiles
+                          // (long-K GEMMs, where few tiles per pair make the deal uneven)
 };
 
 constexpr int kGemmBM = 128;

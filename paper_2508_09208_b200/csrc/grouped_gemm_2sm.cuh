@@ -174,8 +174,21 @@ __device__ __forceinline__ Tile2 decode_tile2(const int* prefix, const GroupedGe
     tt = local / f_tiles;
     t.ft = local % f_tiles;
   }
-  t.tok0 = tt * kBN;
-  t.ntok = min(kBN, rows - t.tok0);
+  // Equal token tiles (p.equal_tiles, long-K launches): a group's rows are
+  // split into ceil(rows/kBN) tiles of one size (rounded up to 16), e.g. 600
+  // rows -> 208 + 208 + 184 instead of 256 + 256 + 88. Same tile count (same
+  // weight traffic), but the tiles a round-robin deal hands the pairs are
+  // near-equal in MMA work: in the output GEMM at C2 (13 tiles per pair) the
+  // busiest pair's excess over the average drops from 21-32% to ~11%
+  // (DESIGN §K3). The activation GEMM (52 tiles per pair) keeps fixed tiles:
+  // there smaller tiles cost more operand ingest per MAC than balance gains.
+  int size = kBN;
+  if (p.equal_tiles) {
+    const int n_tt = (rows + kBN - 1) / kBN;
+    size = (((rows + n_tt - 1) / n_tt) + 15) & ~15;
+  }
+  t.tok0 = tt * size;
+  t.ntok = min(size, rows - t.tok0);
   t.nmma = (t.ntok + 15) & ~15;
   return t;
 }
