@@ -184,7 +184,7 @@ __device__ __forceinline__ Tile2 decode_tile2(const int* prefix, const GroupedGe
   // there smaller tiles cost more operand ingest per MAC than balance gains.
   int size = kBN;
   if (p.equal_tiles) {
-    const int n_tt = (rows + kBN - 1) / kBN;
+    const int n_tt = max(1, (rows + kBN - 1) / kBN);  // (a decoded tile's group has rows > 0)
     size = (((rows + n_tt - 1) / n_tt) + 15) & ~15;
   }
   t.tok0 = tt * size;
