@@ -158,7 +158,7 @@ struct Tile2 {
   int g, ft, tok0, ntok, nmma;
 };
 
-template <int kBN>
+template <int kBN, bool kChunk32 = false>
 __device__ __forceinline__ Tile2 decode_tile2(const int* prefix, const GroupedGemmParams& p,
                                               int f_tiles, int tile) {
   Tile2 t;
@@ -184,8 +184,12 @@ __device__ __forceinline__ Tile2 decode_tile2(const int* prefix, const GroupedGe
   // there smaller tiles cost more operand ingest per MAC than balance gains.
   int size = kBN;
   if (p.equal_tiles) {
+    // bulk-store epilogues: sizes in whole 32-token chunks, so every tile but
+    // a group's last keeps the TMA store path (a partial chunk falls back to
+    // 16-byte stores); the scatter epilogue stores rows anyway: 16
     const int n_tt = max(1, (rows + kBN - 1) / kBN);  // (a decoded tile's group has rows > 0)
-    size = (((rows + n_tt - 1) / n_tt) + 15) & ~15;
+    const int q = kChunk32 ? 31 : 15;
+    size = min(kBN, (((rows + n_tt - 1) / n_tt) + q) & ~q);
   }
   t.tok0 = tt * size;
   t.ntok = min(size, rows - t.tok0);
@@ -266,7 +270,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k
     int stage = 0;
     uint32_t phase = 0;
     for (int tile = cluster; tile < total_tiles; tile += n_clusters) {
-      const Tile2 t = decode_tile2<kBN>(prefix, p, f_tiles, tile);
+      const Tile2 t = decode_tile2<kBN, kMode != kEpiScaleScatter>(prefix, p, f_tiles, tile);
       // (dev attribution: debug 16 = every tile loads slot 0 and token row 0,
       // 128 = slot 0 only — L2-resident operands; +27-42% / +17% at C2)
       const int slot = (p.debug & (16 | 128)) ? 0 : __ldg(p.group_slot + t.g);
@@ -319,7 +323,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k
       uint32_t phase = 0;
       int it = 0;
       for (int tile = cluster; tile < total_tiles; tile += n_clusters, ++it) {
-        const Tile2 t = decode_tile2<kBN>(prefix, p, f_tiles, tile);
+        const Tile2 t = decode_tile2<kBN, kMode != kEpiScaleScatter>(prefix, p, f_tiles, tile);
         const uint32_t idesc = umma_idesc_bf16_f32(k2BM, t.nmma);
         const int acc = it & 1;
         mbar_wait(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
@@ -356,7 +360,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<k2Stages, k
     // chunks of one tile handled by this warp (ci = sub, sub + kSubs, ...)
     constexpr int kMaxIt = (kBN / 32 + kSubs - 1) / kSubs;
     for (int tile = cluster; tile < total_tiles; tile += n_clusters, ++it) {
-      const Tile2 t = decode_tile2<kBN>(prefix, p, f_tiles, tile);
+      const Tile2 t = decode_tile2<kBN, kMode != kEpiScaleScatter>(prefix, p, f_tiles, tile);
       const int acc = it & 1;
       const long row_base = static_cast<long>(__ldg(p.group_row_base + t.g)) + t.tok0;
       const long col0 = static_cast<long>(t.ft) * k2BM + rank * 128 + q * 32;
