@@ -881,9 +881,12 @@ template <int EP, bool kPair, int kTerms>
 static int launch_gate_terms(const CUtensorMap& tx, const CUtensorMap& tw, const GateParams& p,
                              cudaStream_t stream) {
   if constexpr (kPair && kTerms == 2) {
+    // 6 ring stages (192 KB of x + router tiles in flight per SM) by default:
+    // the load stream is bound by bytes in flight, ~4.3 vs ~5.0 µs per unit
+    // (profiles/r2_gate_stages_ab.jsonl); COMOE_GATE_STAGES=5 for A/B
     static const bool six = [] {
       const char* e = std::getenv("COMOE_GATE_STAGES");
-      return e && e[0] == '6';
+      return !(e && e[0] == '5');
     }();
     return six ? launch_gate_stages<EP, kPair, kTerms, 6>(tx, tw, p, stream)
                : launch_gate_stages<EP, kPair, kTerms, 5>(tx, tw, p, stream);
