@@ -191,10 +191,13 @@ __global__ void __launch_bounds__(kGateThreads, 1)
     for (int b = 0; b < 2; ++b) {
       mbar_init(&stash_full[b], 128);
       mbar_init(&stash_empty[b], 256);
-      mbar_init(&own_full[b], 8);
-      mbar_init(&own_empty[b], 4);
-      mbar_init(&xch_full[b], 8);
-      mbar_init(&xch_empty[b], 4);
+      // every thread that writes or reads an exchange slot arrives itself
+      // (a lane-0 arrive after __syncwarp is also ordered, but this form is
+      // the one compute-sanitizer racecheck models)
+      mbar_init(&own_full[b], 256);
+      mbar_init(&own_empty[b], 128);
+      mbar_init(&xch_full[b], 256);
+      mbar_init(&xch_empty[b], 128);
     }
     fence_barrier_init();
   }
@@ -348,11 +351,8 @@ __global__ void __launch_bounds__(kGateThreads, 1)
       mbar_wait_cluster(&xch_full[b], par);
       TmPart a = tm_part_load(own + (b * 128 + ft) * 8);
       const TmPart c = tm_part_load(xch + (b * 128 + ft) * 8);
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&own_empty[b]);
-        mbar_arrive_remote_release(mapa_u32(smem_u32(&xch_empty[b]), 1));
-      }
+      mbar_arrive(&own_empty[b]);
+      mbar_arrive_remote_release(mapa_u32(smem_u32(&xch_empty[b]), 1));
       tm_part_merge(a, c, need_sum);  // SM0's experts have the lower ids
       const float s = need_sum ? a.s : 1.f;
       const int t = fu * kGemmBM + ft;
@@ -522,16 +522,14 @@ __global__ void __launch_bounds__(kGateThreads, 1)
                        "r"(__float_as_uint(pa.m)), "r"(__float_as_uint(pa.s))
                        : "memory");
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive_remote_release(mapa_u32(smem_u32(&xch_full[buf]), 0));
+        mbar_arrive_remote_release(mapa_u32(smem_u32(&xch_full[buf]), 0));
         if (lane == 0 && w8 == 0) gate_tl(p, tl0, 17, u);
         continue;
       }
       // SM0: own partials for the lagged finalisation
       mbar_wait(&own_empty[buf], par ^ 1);
       if (lo) tm_part_store(own + (buf * 128 + tt) * 8, pa);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&own_full[buf]);
+      mbar_arrive(&own_full[buf]);
       if (!drain && prev_u >= 0) finalize(prev_u, it - 1);
       prev_u = u;
     }
